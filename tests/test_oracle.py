@@ -1,0 +1,465 @@
+"""Pins for the CPU oracle (oracle/ddl_oracle.py) against things other than itself:
+the plain definition (naive rank-by-rank sum), closed forms of rank-indexed
+inputs, hand-derived worked examples (tests/golden/worked_examples.json), a brute-force
+scalar evaluator of the nested fold formula (no buffers, blocks or phases), library bf16
+casts, the Higham error bound, and the SPEC's invariants.
+
+A plausible oracle mistake -- a dropped term, a wrong group member or coordinate, a
+transposed fold order, a missing phase-boundary rounding, a misplaced avg multiply, a
+wrong block range -- fails at least one of these.  CPU only (no GPU marker).
+"""
+import itertools
+import json
+import math
+import os
+import struct
+
+import ml_dtypes
+import numpy as np
+import pytest
+import torch
+from hypothesis import given, settings, strategies as st, HealthCheck
+
+import oracle
+import synthetic_inputs as si
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")
+
+
+def factorisations(P, maxlen=4):
+    """Every ordered factorisation of P into factors >= 2 (plus [1] for P = 1)."""
+    if P == 1:
+        return [[1]]
+    out = []
+
+    def rec(rem, cur):
+        if rem == 1:
+            out.append(list(cur))
+            return
+        if len(cur) >= maxlen:
+            return
+        for f in range(2, rem + 1):
+            if rem % f == 0:
+                rec(rem // f, cur + [f])
+    rec(P, [])
+    return out
+
+
+def same_bits(a, b):
+    """Bitwise equality, except every NaN equals every NaN (ledger 10)."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if a.dtype == np.float32:
+        na, nb = np.isnan(a), np.isnan(b)
+        return bool(np.array_equal(na, nb) and np.array_equal(a.view(np.uint32)[~na], b.view(np.uint32)[~nb]))
+    return bool(np.array_equal(a, b))
+
+
+# --------------------------------------------------------------------------- brute force
+# An independent scalar evaluator of the nested formula
+#   S_{d+1}(c_{d+1..}) = fold_{c_d = 0..g_d-1} S_d(c_d, c_{d+1..})
+# (SURVEY.md 8(c) "Fold order"): pure Python numbers, one element at a time, rounding done
+# with struct (binary32) and ml_dtypes (bfloat16) instead of numpy array arithmetic.  For
+# binary32 + and *, computing in binary64 and rounding once is exact-then-rounded because
+# 53 >= 2*24 + 2 (double rounding is innocuous).
+
+def fl32(x: float) -> float:
+    return struct.unpack("<f", struct.pack("<f", x))[0]
+
+
+def flbf16(x: float) -> float:
+    return float(ml_dtypes.bfloat16(np.float32(x)))
+
+
+def brute_element(vals, dims, dtype, op):
+    P = len(vals)
+    if dtype == "int32":
+        level = [int(v) for v in vals]
+    elif dtype == "bfloat16":
+        level = [float(np.uint32(int(v) << 16).view(np.float32)) for v in vals]
+    else:
+        level = [float(v) for v in vals]
+    live = [d for d, g in enumerate(dims) if g > 1]
+    for d, g in enumerate(dims):
+        if g == 1:
+            continue
+        nxt = []
+        for i in range(len(level) // g):
+            grp = level[i * g:(i + 1) * g]        # ranks sharing coords > d, ascending c_d
+            acc = grp[0]
+            for v in grp[1:]:
+                acc = ((acc + v + 2**31) % 2**32) - 2**31 if dtype == "int32" else fl32(acc + v)
+            if op == "avg" and d == live[-1]:
+                acc = fl32(acc * fl32(1.0 / P))
+            if dtype == "bfloat16":
+                acc = flbf16(acc)
+            nxt.append(acc)
+        level = nxt
+    (y,) = level
+    if dtype == "int32":
+        return np.int32(y)
+    if dtype == "bfloat16":
+        return ml_dtypes.bfloat16(y).view(np.uint16)
+    return np.float32(y)
+
+
+def brute_allreduce(bufs, dims, dtype, op):
+    n = len(bufs[0])
+    return np.array([brute_element([b[e] for b in bufs], dims, dtype, op) for e in range(n)],
+                    dtype=oracle.ddl_oracle.STORAGE[dtype])
+
+
+# --------------------------------------------------------------------------- topology / schedule
+
+def test_parse_dims_outer_by_inner():
+    assert oracle.parse_dims("2x4") == [4, 2]
+    assert oracle.parse_dims("2x2x2") == [2, 2, 2]
+    assert oracle.parse_dims("8") == [8]
+    assert oracle.parse_dims([4, 2]) == [4, 2]
+
+
+def test_golden_schedules_and_bad_dims():
+    g = json.load(open(GOLDEN))
+    for s in g["schedules"]:
+        dims = oracle.parse_dims(s["spec"]) if "spec" in s else s["dims"]
+        assert dims == s["dims"], s["cite"]
+        assert [list(p) for p in oracle.schedule(dims)] == s["expect"], s["cite"]
+    for b in g["bad_dims"]:
+        with pytest.raises(oracle.BadDims):
+            oracle.validate_dims(b["dims"], b["nranks"])
+
+
+def test_golden_tier_between():
+    # tier_between(a, b) = innermost dim whose coordinate differs
+    for t in json.load(open(GOLDEN))["tier_between"]:
+        dims = t["dims"]
+        diff = [d for d in range(len(dims)) if oracle.coord(t["a"], d, dims) != oracle.coord(t["b"], d, dims)]
+        assert max(diff) == t["tier"], t["cite"]
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 6, 8, 12, 16, 24, 32])
+def test_coords_mixed_radix_roundtrip(P):
+    for dims in factorisations(P):
+        G = [math.prod(dims[:d]) for d in range(len(dims))]
+        for r in range(P):
+            c = [oracle.coord(r, d, dims) for d in range(len(dims))]
+            assert sum(ci * Gi for ci, Gi in zip(c, G)) == r          # S:L294 bijection
+            for d in range(len(dims)):
+                grp = oracle.group(r, d, dims)
+                assert len(grp) == dims[d] and r in grp
+                assert [oracle.coord(m, d, dims) for m in grp] == list(range(dims[d]))
+                for m in grp:   # a group differs from r only in coordinate d
+                    assert all(oracle.coord(m, j, dims) == c[j] for j in range(len(dims)) if j != d)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 6, 8, 12])
+def test_active_blocks_end_at_own_block(P):
+    """After all RS phases rank r owns exactly block r; |A_d| = P / G_d."""
+    for dims in factorisations(P):
+        k = len(dims)
+        for r in range(P):
+            assert oracle.active_blocks(r, k, dims) == [r]
+            for d in range(k + 1):
+                assert len(oracle.active_blocks(r, d, dims)) == P // math.prod(dims[:d])
+        # within an RS phase, the blocks a rank writes are disjoint from those its group reads from it
+        for d in range(k):
+            for r in range(P):
+                mine = set(oracle.active_blocks(r, d + 1, dims))
+                for m in oracle.group(r, d, dims):
+                    if m != r:
+                        assert mine.isdisjoint(oracle.active_blocks(m, d + 1, dims))
+
+
+# --------------------------------------------------------------------------- worked examples
+
+def test_golden_worked_examples():
+    for ex in json.load(open(GOLDEN))["examples"]:
+        dt = ex["dtype"]
+        if dt == "bfloat16":
+            bufs = [np.array([int(h, 16) for h in x], dtype=np.uint16) for x in ex["inputs_hex"]]
+            want = np.array([int(h, 16) for h in ex["expect_all_ranks_hex"]], dtype=np.uint16)
+        else:
+            st_ = oracle.ddl_oracle.STORAGE[dt]
+            bufs = [np.array(x, dtype=st_) for x in ex["inputs"]]
+            want = np.array(ex["expect_all_ranks"], dtype=st_)
+        out = oracle.allreduce(bufs, ex["dims"], dt, ex["op"])
+        for r, y in enumerate(out):
+            assert same_bits(y, want), (ex["name"], ex["cite"], r, y, want)
+        # and the brute-force evaluator agrees with the hand derivation too
+        assert same_bits(brute_allreduce(bufs, ex["dims"], dt, ex["op"]), want), ex["name"]
+
+
+# --------------------------------------------------------------------------- int32: exact
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 6, 8])
+@pytest.mark.parametrize("kind", ["uniform", "fullrange"])
+def test_int32_equals_naive_sum(P, kind):
+    n = 1003
+    bufs = si.rank_buffers("int32", kind, n, P)
+    want = oracle.naive_sum(bufs, "int32")
+    for dims in factorisations(P):
+        out = oracle.allreduce(bufs, dims, "int32")
+        for y in out:
+            assert np.array_equal(y, want), dims
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_int32_bitmask_closed_form(P):
+    n = (1 << 20) + 37      # wraps the (i mod 2^20) field once
+    bufs = si.rank_buffers("int32", "bitmask", n, P)
+    i = np.arange(n, dtype=np.int64)
+    want = (((1 << P) - 1) + P * ((i % (1 << 20)) << 8)) & 0xFFFFFFFF
+    want = want.astype(np.uint32).view(np.int32)
+    for dims in factorisations(P):
+        for y in oracle.allreduce(bufs, dims, "int32"):
+            assert np.array_equal(y, want), dims
+
+
+def test_int32_wrap():
+    bufs = [np.full(5, 1 << 30, dtype=np.int32) for _ in range(4)]
+    for dims in ([4], [2, 2]):
+        for y in oracle.allreduce(bufs, dims, "int32"):
+            assert np.all(y == 0)
+
+
+def test_int32_avg_rejected():
+    with pytest.raises(oracle.Unsupported):
+        oracle.allreduce([np.zeros(4, np.int32)] * 2, [2], "int32", "avg")
+
+
+# --------------------------------------------------------------------------- fp32
+
+@pytest.mark.parametrize("P", [2, 3, 4, 6, 8])
+def test_fp32_intvalued_exact(P):
+    bufs = si.rank_buffers("float32", "intvalued", 777, P)
+    s64, _ = oracle.exact_sum_f64(bufs, "float32")
+    for dims in factorisations(P):
+        for y in oracle.allreduce(bufs, dims, "float32"):
+            assert np.array_equal(y.astype(np.float64), s64), dims
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8, 16])
+def test_fp32_rankplus1_closed_form(P):
+    bufs = si.rank_buffers("float32", "rankplus1", 100, P)
+    for dims in factorisations(P):
+        assert np.all(oracle.allreduce(bufs, dims, "float32")[P - 1] == P * (P + 1) / 2)
+        assert np.all(oracle.allreduce(bufs, dims, "float32", "avg")[0] == (P + 1) / 2)
+
+
+@pytest.mark.parametrize("P", [2, 3, 5, 8])
+def test_fp32_flat_dims_is_recursive_summation(P):
+    """dims = [P] is textbook recursive summation in ascending rank: bitwise equal to a
+    plain float32 left fold (the naive definition)."""
+    bufs = si.rank_buffers("float32", "normal", 4099, P)
+    want = oracle.naive_sum(bufs, "float32")
+    acc = bufs[0].copy()
+    for x in bufs[1:]:
+        acc = (acc + x).astype(np.float32)
+    assert np.array_equal(want, acc)
+    for y in oracle.allreduce(bufs, [P], "float32"):
+        assert same_bits(y, want)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8, 16])
+def test_fp32_higham_bound(P):
+    """|y - s| <= gamma_{P-1} * sum_r |x_r| for any summation order (Higham, recursive
+    summation / any tree), gamma_m = m u / (1 - m u), u = 2^-24."""
+    bufs = si.rank_buffers("float32", "normal", 20000, P)
+    s64, a64 = oracle.exact_sum_f64(bufs, "float32")
+    u = 2.0 ** -24
+    gam = (P - 1) * u / (1 - (P - 1) * u)
+    for dims in factorisations(P):
+        y = oracle.allreduce(bufs, dims, "float32")[0].astype(np.float64)
+        assert np.all(np.abs(y - s64) <= gam * a64 + 1e-45), dims
+        assert np.max(np.abs(y - s64) / a64) < 1e-6       # north_star fp32 tolerance (ledger 8)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_avg_power_of_two_equals_sum_then_scale(P):
+    """For P = 2^m, x * 2^-m is exact: fused avg == SPEC's sum-then-scale."""
+    bufs = si.rank_buffers("float32", "normal", 3001, P)
+    for dims in factorisations(P):
+        s = oracle.allreduce(bufs, dims, "float32", "sum")[0]
+        a = oracle.allreduce(bufs, dims, "float32", "avg")[0]
+        assert np.array_equal(a, (s * np.float32(1.0 / P)).astype(np.float32))
+        assert np.array_equal(a, (s / np.float32(P)).astype(np.float32))
+
+
+# --------------------------------------------------------------------------- bf16
+
+def test_bf16_round_matches_libraries():
+    specials = np.array([0.0, -0.0, 1.0, -1.0, 1 + 2**-8, 1 + 3 * 2**-8, 1 + 2**-7 + 2**-8,
+                         np.finfo(np.float32).max, -np.finfo(np.float32).max, 3.3895e38, 3.4e38,
+                         np.inf, -np.inf, 1e-40, -1e-40, 2**-133, 1.17549435e-38, 65504.0,
+                         np.float32(1.00390625), 255.5, 256.5], dtype=np.float32)
+    r = oracle.ddl_oracle.rng if False else None  # noqa: F841  (no oracle RNG; inputs below)
+    rnd = np.random.Generator(np.random.PCG64(7))
+    bits = rnd.integers(0, 1 << 32, size=200000, dtype=np.uint32)
+    bits = bits[((bits >> 23) & 0xFF) != 0xFF]                       # finite patterns
+    x = np.concatenate([specials, bits.view(np.float32), rnd.standard_normal(50000).astype(np.float32)])
+    mine = oracle.bf16_round(x)
+    ml = x.astype(ml_dtypes.bfloat16).view(np.uint16)
+    th = torch.from_numpy(x.copy()).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(mine, ml)
+    assert np.array_equal(mine, th)
+    nan_in = np.array([np.nan, -np.nan, np.uint32(0x7F800001).view(np.float32)], dtype=np.float32)
+    assert np.all(np.isnan(oracle.bf16_to_f32(oracle.bf16_round(nan_in))))
+    back = oracle.bf16_to_f32(mine)
+    assert np.array_equal(back, ml.view(ml_dtypes.bfloat16).astype(np.float32), equal_nan=True)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_bf16_error_bound(P):
+    """Each phase boundary rounds to bf16 (relative 2^-8 of a partial bounded by sum|x|):
+    |y - s| <= (k * 2^-8 + (P-1) * 2^-24 * (1 + 2^-8)^k) * sum|x| + tiny."""
+    bufs = si.rank_buffers("bfloat16", "normal", 50000, P)
+    s64, a64 = oracle.exact_sum_f64(bufs, "bfloat16")
+    for dims in factorisations(P):
+        k = len(dims)
+        y = oracle.bf16_to_f32(oracle.allreduce(bufs, dims, "bfloat16")[0]).astype(np.float64)
+        bound = (k * 2.0**-8 + (P - 1) * 2.0**-24 * (1 + 2.0**-8) ** k) * (1 + 2.0**-8) ** k
+        assert np.all(np.abs(y - s64) <= bound * a64 + 1e-38), dims
+        assert np.max(np.abs(y - s64) / np.maximum(a64, 1e-30)) <= 1e-2 + 2e-3 * (k - 1), dims
+
+
+# --------------------------------------------------------------------------- brute-force nested fold
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 6, 8])
+@pytest.mark.parametrize("dtype,kind", [("float32", "normal"), ("bfloat16", "normal"), ("int32", "fullrange")])
+def test_nested_formula_brute_force(P, dtype, kind):
+    n = 37     # spans several blocks and a ragged tail for every P here
+    bufs = si.rank_buffers(dtype, kind, n, P)
+    for dims in factorisations(P):
+        for op in (["sum"] if dtype == "int32" else ["sum", "avg"]):
+            want = brute_allreduce(bufs, dims, dtype, op)
+            out = oracle.allreduce(bufs, dims, dtype, op)
+            for y in out:
+                assert same_bits(y, want), (dims, op)
+
+
+def test_nested_formula_brute_force_32_ranks():
+    for P, dims in [(32, [2, 4, 4]), (32, [8, 4]), (24, [3, 2, 4]), (16, [2, 2, 2, 2])]:
+        bufs = si.rank_buffers("float32", "normal", 19, P)
+        assert same_bits(oracle.allreduce(bufs, dims, "float32", "avg")[P - 1],
+                         brute_allreduce(bufs, dims, "float32", "avg"))
+        bb = si.rank_buffers("bfloat16", "normal", 19, P)
+        assert same_bits(oracle.allreduce(bb, dims, "bfloat16")[3], brute_allreduce(bb, dims, "bfloat16", "sum"))
+
+
+@settings(max_examples=500, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.integers(1, 32).flatmap(lambda P: st.tuples(st.just(P), st.sampled_from(factorisations(P, 5)))),
+       st.integers(0, 300), st.integers(0, 2**31 - 1))
+def test_property_spec_acceptance_5(Pdims, n, seed):
+    """random (topology, buffer) instances up to 32 ranks, integer-valued:
+    hierarchical == brute-force sum == flat (dims [P]) result."""
+    P, dims = Pdims
+    bufs = si.rank_buffers("float32", "intvalued", n, P, seed=seed)
+    s64, _ = oracle.exact_sum_f64(bufs, "float32")
+    h = oracle.allreduce(bufs, dims, "float32")
+    f = oracle.allreduce(bufs, [P], "float32")
+    for y in h:
+        assert np.array_equal(y.astype(np.float64), s64)
+    assert np.array_equal(h[0], f[P - 1])
+
+
+# --------------------------------------------------------------------------- invariants
+
+@pytest.mark.parametrize("P,n", [(4, 1_000_003), (8, 5), (8, 7), (8, 1), (3, 2), (4, 0)])
+def test_ragged_and_degenerate(P, n):
+    """S:L369 padding transparency: output length = input length; n < P leaves empty blocks."""
+    bufs = si.rank_buffers("int32", "uniform", n, P)
+    want = oracle.naive_sum(bufs, "int32")
+    for dims in factorisations(P)[:3]:
+        out = oracle.allreduce(bufs, dims, "int32")
+        assert all(len(y) == n for y in out)
+        assert all(np.array_equal(y, want) for y in out)
+
+
+@pytest.mark.parametrize("dtype,kind", [("float32", "normal"), ("bfloat16", "normal")])
+def test_replicas_identical_and_deterministic(dtype, kind):
+    """S:L441 replica consistency; S:L368 order-fixity (two runs bitwise identical)."""
+    P = 8
+    bufs = si.rank_buffers(dtype, kind, 2053, P)
+    for dims in factorisations(P):
+        a = oracle.allreduce(bufs, dims, dtype, "avg")
+        b = oracle.allreduce(bufs, dims, dtype, "avg")
+        for r in range(P):
+            assert same_bits(a[r], a[0]) and same_bits(a[r], b[r])
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_reduce_scatter_allgather_compose(P):
+    """allgather(reduce_scatter(x)) == allreduce(x); RS slice r == allreduce block r."""
+    q = 96                                   # a multiple of the 16-B vector -> same layout
+    for dtype, kind in [("float32", "normal"), ("bfloat16", "normal"), ("int32", "fullrange")]:
+        bufs = si.rank_buffers(dtype, kind, P * q, P)
+        for dims in factorisations(P):
+            ops = ["sum"] if dtype == "int32" else ["sum", "avg"]
+            for op in ops:
+                ar = oracle.allreduce(bufs, dims, dtype, op)
+                rs = oracle.reduce_scatter(bufs, dims, dtype, op)
+                for r in range(P):
+                    assert same_bits(rs[r], ar[r][r * q:(r + 1) * q])
+                ag = oracle.allgather(rs, dims, dtype)
+                for r in range(P):
+                    assert same_bits(ag[r], ar[r])
+
+
+def test_allgather_is_concatenation():
+    P = 8
+    sends = [np.arange(10, dtype=np.int32) + 100 * r for r in range(P)]
+    for dims in factorisations(P):
+        for y in oracle.allgather(sends, dims, "int32"):
+            assert np.array_equal(y, np.concatenate(sends))
+
+
+def test_int32_dims_permutation_invariant():
+    P = 8
+    bufs = si.rank_buffers("int32", "fullrange", 999, P)
+    res = {tuple(d): oracle.allreduce(bufs, d, "int32")[0] for d in factorisations(P)}
+    first = next(iter(res.values()))
+    assert all(np.array_equal(v, first) for v in res.values())
+
+
+def test_sampled_equals_full():
+    P = 8
+    n = 5000
+    rnd = np.random.Generator(np.random.PCG64(3))
+    idx = np.sort(rnd.choice(n, 300, replace=False))
+    for dtype in ("float32", "bfloat16"):
+        bufs = si.rank_buffers(dtype, "normal", n, P)
+        for dims in ([4, 2], [2, 2, 2], [8]):
+            full = oracle.allreduce(bufs, dims, dtype, "avg")[5]
+            assert same_bits(oracle.allreduce_sampled(bufs, dims, dtype, "avg", idx), full[idx])
+
+
+# --------------------------------------------------------------------------- traffic
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_traffic_conservation(P):
+    n = P * 64
+    S = n * 4
+    for dims in factorisations(P):
+        t = oracle.Traffic.new(P)
+        oracle.allreduce(si.rank_buffers("float32", "normal", n, P), dims, "float32", traffic=t)
+        for r in range(P):
+            assert sum(t.remote_read[r].values()) == 2 * (P - 1) * S // P
+            for d, g in enumerate(dims):
+                active = S // math.prod(dims[:d])
+                assert t.remote_read[r][("RS", d)] == (g - 1) * active // g
+                assert t.remote_read[r][("AG", d)] == (g - 1) * active // g
+
+
+# --------------------------------------------------------------------------- K5 local reduce
+
+def test_local_reduce():
+    ins = si.rank_buffers("int32", "fullrange", 1000, 8)
+    assert np.array_equal(oracle.local_reduce(ins, "int32"), oracle.naive_sum(ins, "int32"))
+    f = si.rank_buffers("float32", "normal", 1000, 5)
+    assert np.array_equal(oracle.local_reduce(f, "float32"), oracle.naive_sum(f, "float32"))
+    iv = si.rank_buffers("float32", "intvalued", 1000, 4)
+    s64, _ = oracle.exact_sum_f64(iv, "float32")
+    assert np.array_equal(oracle.local_reduce(iv, "float32", 0.25).astype(np.float64), s64 / 4)
+    b = si.rank_buffers("bfloat16", "normal", 1000, 4)
+    want = oracle.bf16_round(oracle.naive_sum(b, "bfloat16"))
+    assert np.array_equal(oracle.local_reduce(b, "bfloat16"), want)
