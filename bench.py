@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Benchmark of the DDL all-reduce (BASELINE.json metric: all-reduce bus GB/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ddl|reference] [--config ...]
+
+One *step* is the whole hot path (every SURVEY.md 8(a) row) over one synchronous-SGD
+gradient set: the BASELINE.json configs[1] workload, ResNet-50's 25.6M fp32 gradients in
+its 5 DDP buckets, all-reduced with op=avg, dims 2x4 (= [4, 2]).
+
+* N = 1 (no torchrun): LOOPBACK -- the 8 ranks of the 2x4 factorisation are virtual ranks
+  on one B200 (one cooperative launch per bucket, the same kernels / block layout / barrier
+  protocol as the multi-GPU path, peer pointers local).  Bound: HBM.
+* N > 1 (torchrun, one process per GPU): real ranks, peers' buffers mapped over NVLink 5 /
+  NVSwitch, dims 8 -> 2x4, 4 -> 2x2, 2 -> 2.  Bound: NVLink.  NCCL's all-reduce on the same
+  buffers is timed alongside (comparison only).
+
+value = bus bandwidth = sum_b S_b * 2(P-1)/P / t_step (NCCL-tests convention; per-rank link
+bandwidth, the figure the metric's "% of 900 GB/s" refers to).  Timing: W untimed warm-up
+steps, then K steps between barrier + synchronize, CUDA events on the launching stream,
+max over ranks.  The gradient set (8 x 102 MB) is larger than the 126 MB L2, so no flush
+is needed between steps.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synthetic_inputs as si  # noqa: E402
+
+METRIC = "allreduce bus GB/s vs msg size at 2/4/8 B200 (% of 900 GB/s NVLink) vs NCCL"
+NVLINK_NOMINAL = 900.0
+NVLINK_MEASURED_PEER = 770.0   # B200_PROFILING.md: measured peer copy per direction
+DIMS_FOR_N = {1: "2x4", 2: "2", 4: "2x2", 8: "2x4"}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workload
+def resnet50_set(rank: int):
+    """The gradient set of one rank: 5 DDP buckets (fp32)."""
+    return [si.resnet50_bucket(b, rank) for b in range(len(si.resnet50_bucket_bytes()))]
+
+
+def loopback_hbm_bytes(n: int, P: int, dims, w: int) -> int:
+    """Algorithmic HBM bytes of one loopback hierarchical all-reduce (all P virtual ranks):
+    per rank, RS phase d reads its g_d group members' copies of the blocks A_{d+1}(r) and
+    writes them once; AG phase d reads (g_d - 1)|A_{d+1}| blocks from peers and writes them.
+    Exact over ragged block lengths."""
+    q = -(-(-(-n // P)) // (16 // w)) * (16 // w)
+    blen = [max(0, min(n, (b + 1) * q) - min(n, b * q)) for b in range(P)]
+    G = [math.prod(dims[:d]) for d in range(len(dims) + 1)]
+    total = 0
+    for r in range(P):
+        for d, g in enumerate(dims):
+            if g == 1:
+                continue
+            own = [b for b in range(P) if b % G[d + 1] == r % G[d + 1]]            # A_{d+1}(r)
+            total += sum(blen[b] for b in own) * (g + 1)                           # RS: g reads + 1 write
+            recv = [b for b in range(P) if b % G[d] == r % G[d] and b not in own]  # AG: blocks received
+            total += sum(blen[b] for b in recv) * 2                                # read + write
+    return total * w
+
+
+# ----------------------------------------------------------------------------- cpu baseline
+def oracle_baseline(P: int, dims, budget_s: float = 12.0):
+    """The oracle as it stands, on a bounded sample of the workload (host cores)."""
+    import oracle
+    n = 4 << 20
+    bufs = [si.resnet50_bucket(1, r)[:n] for r in range(P)]
+    S = n * 4
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.allreduce(bufs, dims, "float32", "avg")
+        reps += 1
+        el = time.perf_counter() - t0
+        if el > budget_s or reps >= 8:
+            break
+    t = el / reps
+    return {"value": S * 2 * (P - 1) / P / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{reps} oracle all-reduce(s) of 4M fp32 elements x {P} simulated ranks "
+                      f"(first 16 MiB of ResNet-50 bucket 1), dims {dims}, avg; numpy single-threaded",
+            "host_cpus": len(os.sched_getaffinity(0))}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the only 'reference' this paper-only tier has), timed on
+    the host cores, each step a bounded sample of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    P, dims = 8, [4, 2]
+    n = 1 << 20
+    bufs = [si.resnet50_bucket(1, r)[:n] for r in range(P)]
+    for _ in range(args.warmup):
+        oracle.allreduce(bufs, dims, "float32", "avg")
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.allreduce(bufs, dims, "float32", "avg")
+    t = (time.perf_counter() - t0) / args.steps
+    val = n * 4 * 2 * (P - 1) / P / t / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "resnet50-grad-set sample: 1M fp32 x 8 simulated ranks, dims 2x4, avg",
+                       "dims": "2x4", "n_ranks": P},
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": "each step: one oracle all-reduce of the first 1M elements of "
+                                       "ResNet-50 bucket 1 on 8 simulated ranks"},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- N = 1: loopback
+def run_loopback(args):
+    import torch
+    from paper_1811_12174_b200 import ddl
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda:0")
+    P = 8
+    dims = ddl.parse_dims(args.dims or DIMS_FOR_N[1])
+    lb = ddl.Loopback(P, dims, device=0)
+    host = [resnet50_set(r) for r in range(P)]                 # [rank][bucket]
+    nb = len(host[0])
+    sizes = [h.size for h in host[0]]
+    bufs = [[torch.from_numpy(host[r][b]).to(dev) for r in range(P)] for b in range(nb)]   # [bucket][rank]
+    S_total = sum(sizes) * 4
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        for b in range(nb):
+            if evs is not None:
+                evs[b][0].record(stream)
+            lb.all_reduce(bufs[b], "avg")
+            if evs is not None:
+                evs[b][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nb)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    ms = t_start.elapsed_time(t_end) / args.steps
+    busbw = S_total * 2 * (P - 1) / P / (ms * 1e-3) / 1e9
+    kern_ms = sum(evs[k][b][0].elapsed_time(evs[k][b][1]) for k in range(args.steps) for b in range(nb))
+    algo_bytes = sum(loopback_hbm_bytes(n, P, dims, 4) for n in sizes) * args.steps
+    hbm_peak, peak_src = peaks()
+    achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
+
+    # e2e through the public API with HOST buffers: per step H2D of every rank's buckets from
+    # pinned memory, the all-reduce, D2H of the reduced gradient set (identical on all ranks).
+    pinned = [[torch.from_numpy(host[r][b]).pin_memory() for r in range(P)] for b in range(nb)]
+    out_host = [torch.empty(s, dtype=torch.float32).pin_memory() for s in sizes]
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step():
+        for b in range(nb):
+            for r in range(P):
+                bufs[b][r].copy_(pinned[b][r], non_blocking=True)
+            lb.all_reduce(bufs[b], "avg")
+            out_host[b].copy_(bufs[b][0], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+
+    # K5: local reduce/scale, g = 8 fp32 buffers of 64 MiB -> out, vs HBM
+    g, n5 = 8, (64 << 20) // 4
+    ins = [torch.randn(n5, device=dev) for _ in range(g)]
+    out5 = torch.empty(n5, device=dev)
+    for _ in range(3):
+        ddl.local_reduce(ins, out5, 1.0 / g)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    k0.record(stream)
+    reps5 = 20
+    for _ in range(reps5):
+        ddl.local_reduce(ins, out5, 1.0 / g)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    k5_ms = k0.elapsed_time(k1) / reps5
+    k5_gbs = (g + 1) * n5 * 4 / (k5_ms * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": busbw, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "resnet50-grad-set (25,557,032 fp32 in 5 DDP buckets) all-reduce avg, "
+                               "8 virtual ranks (loopback on 1 B200), dims 2x4",
+                   "dims": "x".join(map(str, dims[::-1])), "n_ranks": P, "bytes_per_rank": S_total,
+                   "buckets": sizes, "l2": "inputs (8 x 102 MB) larger than L2, no flush",
+                   "algo": ["oneshot" if lb.algo_for(s, "float32") == ddl.ALGO_ONESHOT else "hier" for s in sizes],
+                   "ctas_per_rank": [lb.ctas_for(s, "float32") for s in sizes]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "peak_source": peak_src,
+                     "kernel": "ddl_hier_kernel<float,true> (loopback, all 8 virtual ranks)",
+                     "algorithmic_bytes_per_step": algo_bytes // args.steps,
+                     "kernel_ms_per_step": kern_ms / args.steps},
+        "e2e": {"value": S_total * 2 * (P - 1) / P / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+                "ms_per_step": e2e_ms, "h2d_bytes_per_step": S_total * P, "d2h_bytes_per_step": S_total},
+        "gpu_launches": nb * args.steps,
+        "clocks": clk.summary(),
+        "local_reduce": {"g": g, "bytes": (g + 1) * n5 * 4, "ms": k5_ms, "achieved": k5_gbs, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": k5_gbs / hbm_peak},
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_baseline(P, dims)
+    print(json.dumps(line), flush=True)
+    lb.finalize()
+
+
+# ----------------------------------------------------------------------------- N > 1
+def run_multi(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1811_12174_b200 import ddl
+
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = world
+    dims = ddl.parse_dims(args.dims or DIMS_FOR_N.get(P, str(P)))
+    host = resnet50_set(rank)
+    sizes = [h.size for h in host]
+    S_total = sum(sizes) * 4
+    comm = ddl.init(dims, max_bytes=S_total + 256 * len(sizes) + (1 << 20))
+    offs, views = 0, []
+    for h in host:                                   # buckets live in the symmetric buffer (zero-copy)
+        v = comm.buffer(h.size, torch.float32, offs)
+        v.copy_(torch.from_numpy(h))
+        views.append(v)
+        offs += (h.size * 4 + 255) // 256 * 256
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for v in views:
+            comm.all_reduce(v, "avg")
+
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([a.elapsed_time(b) / steps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(local) as clk:
+        ms = timed(step, args.steps)
+    assert comm.async_error() == ddl.SUCCESS
+    busbw = S_total * 2 * (P - 1) / P / (ms * 1e-3) / 1e9
+
+    nccl_bufs = [torch.from_numpy(h).cuda() for h in host]
+
+    def nccl_step():
+        for t in nccl_bufs:
+            dist.all_reduce(t, op=dist.ReduceOp.AVG)
+    for _ in range(args.warmup):
+        nccl_step()
+    nccl_ms = timed(nccl_step, args.steps)
+
+    # e2e: host gradients -> device (pinned H2D), all-reduce, reduced gradients -> host
+    pinned = [torch.from_numpy(h).pin_memory() for h in host]
+    outh = [torch.empty(s).pin_memory() for s in sizes]
+
+    def e2e_step():
+        for v, ph, oh in zip(views, pinned, outh):
+            v.copy_(ph, non_blocking=True)
+            comm.all_reduce(v, "avg")
+            oh.copy_(v, non_blocking=True)
+    e2e_step()
+    e2e_ms = timed(e2e_step, max(3, min(args.steps, 10)))
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": busbw, "unit": "GB/s", "n_gpus": P, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"resnet50-grad-set all-reduce avg, {P} ranks (1 per GPU), dims "
+                                   + "x".join(map(str, dims[::-1])),
+                       "dims": "x".join(map(str, dims[::-1])), "n_ranks": P, "bytes_per_rank": S_total,
+                       "buckets": sizes, "l2": "102 MB per rank, read remotely over NVLink (no L2 reuse)"},
+            "roofline": {"bound": "nvlink", "achieved": busbw, "peak": NVLINK_MEASURED_PEER,
+                         "unit": "GB/s", "frac": busbw / NVLINK_MEASURED_PEER, "traffic": None,
+                         "frac_of_nominal_900": busbw / NVLINK_NOMINAL,
+                         "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)"},
+            "nccl": {"value": S_total * 2 * (P - 1) / P / (nccl_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": nccl_ms},
+            "e2e": {"value": S_total * 2 * (P - 1) / P / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": S_total, "d2h_bytes_per_step": S_total},
+            "gpu_launches": len(sizes) * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    comm.finalize()
+    dist.destroy_process_group()
+
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ddl", choices=["ddl", "reference"])
+    ap.add_argument("--dims", default=None, help="override the factorisation, e.g. 2x2x2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        run_multi(args)
+    else:
+        run_loopback(args)
+
+
+if __name__ == "__main__":
+    main()

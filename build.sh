@@ -1,0 +1,10 @@
+#!/bin/bash
+# Build libddl.so for sm_100a (cross-compiles without a GPU).
+set -euo pipefail
+cd "$(dirname "$0")"
+OUT=paper_1811_12174_b200/libddl.so
+nvcc -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
+  -fmad=false -Xptxas -v -Xcompiler -fPIC,-Wall -shared -cudart static \
+  -Iinclude -Ipaper_1811_12174_b200/csrc \
+  paper_1811_12174_b200/csrc/ddl_host.cu -o "$OUT" "$@"
+echo "built $OUT"

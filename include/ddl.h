@@ -1,0 +1,192 @@
+/*
+ * ddl.h -- C ABI of libddl: PowerAI DDL's topology-aware gradient all-reduce, rebuilt
+ * B200-native (hand-written sm_100a kernels reading peer GPUs' memory over NVLink 5 /
+ * NVSwitch, device-side flag barriers).
+ *
+ * The operation (§2.1): synchronous-SGD all-reduce "decompose[d] ...
+ * into a series of reduce-scatter and all-gather patterns in a topology-aware fashion".
+ * The ranks are factorised as dims = {g_0, ..., g_{k-1}}, INNERMOST FIRST (prod = nranks;
+ * "2x4" = 2 outer x 4 inner = {4, 2}); coordinates c_d(r) = floor(r / G_d) mod g_d with
+ * G_d = prod_{j<d} g_j.  Reduce-scatter phases run d = 0..k-1, then
+ * all-gather phases d = k-1..0.  A dim with g_d = 1 has no phase.
+ *
+ * Results (identical on every rank): y[e] = F_dims(x_0[e], ..., x_{P-1}[e]) where F folds
+ * each dim's group in ascending coordinate, innermost dim first:
+ *   int32    two's-complement wrapping sum (exact; equals the plain sum in any order)
+ *   float32  every add IEEE round-to-nearest-even, no FMA, no flush-to-zero
+ *   bfloat16 fp32 adds within a phase, RNE to bf16 at every phase boundary
+ *   DDL_AVG  one multiply by fl32(1/P) of the fully reduced fp32 value, fused into the
+ *            last reduce-scatter phase (before the output cast); int32 + AVG unsupported.
+ * The result never depends on the algorithm chosen (hierarchical or one-shot) -- see
+ * DESIGN.md "Readings" for every reading of the paper behind these rules.
+ *
+ * Block layout: count elements are split into P blocks of q elements,
+ * q = roundup(ceil(count/P), 16 B / sizeof(elem)); block b = [min(n,bq), min(n,(b+1)q)).
+ * After the reduce-scatter phases rank r holds block r.
+ *
+ * Conventions for every call below:
+ *   - Buffers are device pointers unless stated; counts are in ELEMENTS.
+ *   - Collective calls are asynchronous on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  Argument errors return synchronously and enqueue
+ *     nothing.  Device-side errors (a peer that never arrives: DDL_ERR_TIMEOUT) are
+ *     sticky and read with ddl_async_error().
+ *   - Every rank calls the same sequence of collectives with equal (count, dtype, op).
+ *   - The caller owns buffers, streams and the comm handle; the library owns its
+ *     workspace, flags and IPC mappings and releases them in ddl_finalize().  No C++
+ *     exception crosses the ABI and the library never aborts the process.
+ *   - Device buffers must be 16-byte aligned (DDL_ERR_INVALID_ARGUMENT otherwise).
+ */
+#ifndef DDL_H
+#define DDL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDL_MAX_RANKS 16   /* ranks per communicator (and virtual ranks in loopback) */
+#define DDL_MAX_DIMS 8
+
+typedef struct ddl_comm* ddl_comm_t;
+
+typedef enum {
+  DDL_SUCCESS = 0,
+  DDL_ERR_INVALID_ARGUMENT = 1, /* null/unaligned pointer, bad enum, bad handle bytes     */
+  DDL_ERR_BAD_DIMS = 2,         /* prod(dims) != nranks, g_d < 1, ndims > 8 (SPEC BadArity) */
+  DDL_ERR_UNSUPPORTED = 3,      /* int32 + AVG, nranks > DDL_MAX_RANKS                     */
+  DDL_ERR_CUDA = 4,             /* a CUDA runtime call failed (no GPU, OOM, launch error)  */
+  DDL_ERR_NO_PEER_ACCESS = 5,   /* a peer GPU is not reachable by P2P                       */
+  DDL_ERR_NOT_CONNECTED = 6,    /* collective called before ddl_connect                     */
+  DDL_ERR_TOO_LARGE = 7,        /* message exceeds the workspace on a staged path           */
+  DDL_ERR_TIMEOUT = 8,          /* (async) a device barrier waited longer than the timeout  */
+  DDL_ERR_MISMATCH = 9          /* handles from ranks with different nranks/dims            */
+} ddl_result_t;
+
+typedef enum { DDL_INT32 = 0, DDL_FLOAT32 = 1, DDL_BFLOAT16 = 2 } ddl_dtype_t;
+typedef enum { DDL_SUM = 0, DDL_AVG = 1 } ddl_op_t;
+
+/* Implementation choice per call ("mix-and-match", P:L54 (3)).  AUTO picks ONESHOT for
+ * messages <= the one-shot threshold, HIER otherwise.  Both compute the same F_dims. */
+typedef enum { DDL_ALGO_AUTO = 0, DDL_ALGO_HIER = 1, DDL_ALGO_ONESHOT = 2 } ddl_algo_t;
+
+/* ------------------------------------------------------------------ host-only helpers */
+/* These never touch the GPU; they expose the planner the kernels use, for tests.       */
+
+int ddl_version(void);                                   /* 100 * major + minor           */
+const char* ddl_result_string(ddl_result_t r);           /* static string, never NULL     */
+const char* ddl_last_error_string(void);                 /* last CUDA failure text (this thread) */
+
+/* Validate a factorisation. */
+ddl_result_t ddl_check_dims(int nranks, const int* dims, int ndims);
+
+/* q, the block size in elements, for an all-reduce of `count` elements (layout above). */
+size_t ddl_block_elems(size_t count, int nranks, ddl_dtype_t dtype);
+
+/* Group of `rank` in dim d: members_out[v] = rank + (v - c_d(rank)) * G_d, v < g_d. */
+ddl_result_t ddl_plan_group(int nranks, const int* dims, int ndims, int rank, int d, int* members_out);
+
+/* A_d(rank) = { b : c_j(b) = c_j(rank) for all j < d }, ascending, d in [0, ndims]:
+ * the blocks `rank` reduces in RS phase d-1 / receives in AG phase d-1.
+ * blocks_out needs room for nranks entries; *nblocks_out = nranks / G_d. */
+ddl_result_t ddl_plan_blocks(int nranks, const int* dims, int ndims, int rank, int d,
+                             int* blocks_out, int* nblocks_out);
+
+/* The device barrier schedule of one hierarchical call (2L+1 barriers, L = number of dims
+ * with g_d > 1): for barrier j, peers_out[j*nranks + i] (i < counts_out[j]) are the ranks
+ * `rank` signals and waits for.  *nbarriers_out = 2L+1 (0 when nranks == 1). */
+ddl_result_t ddl_plan_barriers(int nranks, const int* dims, int ndims, int rank,
+                               int* peers_out, int* counts_out, int* nbarriers_out);
+
+/* Bytes `rank` reads from peers in each phase of an all-reduce of `count` elements:
+ * rs_out[d], ag_out[d] for d < ndims (0 for dims with g_d = 1).  SPEC S:L371. */
+ddl_result_t ddl_plan_traffic(size_t count, ddl_dtype_t dtype, int nranks, const int* dims, int ndims,
+                              int rank, uint64_t* rs_out, uint64_t* ag_out);
+
+/* ------------------------------------------------------------------ multi-process comm */
+/* One process per GPU.  Bootstrap: ddl_init -> ddl_export_handle -> (caller all-gathers
+ * the handles, e.g. torch.distributed.all_gather_object) -> ddl_connect(all, rank order).
+ * The handle bytes carry a cudaIpc memory handle of this rank's flag+workspace block. */
+
+ddl_result_t ddl_init(ddl_comm_t* comm, int rank, int nranks, const int* dims, int ndims,
+                      int cuda_device, size_t max_bytes);
+size_t ddl_handle_size(void);
+ddl_result_t ddl_export_handle(ddl_comm_t comm, void* out /* ddl_handle_size() bytes */);
+ddl_result_t ddl_connect(ddl_comm_t comm, const void* all_handles /* nranks * handle_size */);
+
+/* The symmetric zero-copy buffer (max_bytes, 256-B aligned).  An all-reduce on a buffer
+ * inside it, at the SAME offset on every rank, reads peers' data in place (no staging). */
+ddl_result_t ddl_buffer(ddl_comm_t comm, void** dev_ptr, size_t* bytes);
+
+/* In-place all-reduce of buf[0, count).  buf inside ddl_buffer(): zero-copy; any other
+ * device buffer: staged through the workspace (count * size <= max_bytes). */
+ddl_result_t ddl_allreduce(ddl_comm_t comm, void* buf, size_t count, ddl_dtype_t dtype,
+                           ddl_op_t op, void* stream);
+
+/* NCCL layout: sendbuf holds nranks * recvcount elements; rank r receives elements
+ * [r*recvcount, (r+1)*recvcount) of the reduced vector.  sendbuf is not modified.
+ * Staged through the workspace: nranks * recvcount * size <= max_bytes. */
+ddl_result_t ddl_reduce_scatter(ddl_comm_t comm, const void* sendbuf, void* recvbuf, size_t recvcount,
+                                ddl_dtype_t dtype, ddl_op_t op, void* stream);
+
+/* Rank r's sendcount elements land at [r*sendcount, (r+1)*sendcount) of every rank's
+ * recvbuf (nranks * sendcount elements).  Staged through the workspace. */
+ddl_result_t ddl_allgather(ddl_comm_t comm, const void* sendbuf, void* recvbuf, size_t sendcount,
+                           ddl_dtype_t dtype, void* stream);
+
+/* Sticky device-side error of this comm (synchronises the device to read it). */
+ddl_result_t ddl_async_error(ddl_comm_t comm);
+
+/* Algorithm override: algo, and the one-shot threshold in bytes (AUTO only). */
+ddl_result_t ddl_set_algo(ddl_comm_t comm, ddl_algo_t algo, size_t oneshot_max_bytes);
+
+/* Barrier-spin timeout in milliseconds (default 10000; env DDL_TIMEOUT_MS). */
+ddl_result_t ddl_set_timeout(ddl_comm_t comm, uint64_t timeout_ms);
+
+/* Algorithm AUTO would use for this message (for tests / bench labelling). */
+ddl_algo_t ddl_algo_for(ddl_comm_t comm, size_t count, ddl_dtype_t dtype);
+
+/* Number of CTAs per rank a call of this size launches. */
+int ddl_ctas_for(ddl_comm_t comm, size_t count, ddl_dtype_t dtype);
+
+/* Test hook: virtual/process rank `rank` skips its part of every following call (-1 = off),
+ * so its peers' barriers time out (DDL_ERR_TIMEOUT via ddl_async_error).  Never use in
+ * production: the skipped rank's data is not reduced. */
+ddl_result_t ddl_debug_skip_rank(ddl_comm_t comm, int rank);
+
+/* Collective teardown: every rank must have finished all calls (host barrier first).
+ * Unmaps peers, frees the workspace, destroys the handle.  NULL is a no-op. */
+ddl_result_t ddl_finalize(ddl_comm_t comm);
+
+/* ------------------------------------------------------------------ loopback (1 GPU) */
+/* P virtual ranks in ONE GPU's memory, all in one cooperative launch (deadlock-free):
+ * the same kernels, barrier protocol and block layout as the multi-process path, with
+ * "peer" pointers that are local.  Used by the parity tests and the 1-GPU benchmark. */
+
+ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, int ndims, int cuda_device);
+
+/* bufs: host array of nranks device pointers (distinct, 16-B aligned, count elements
+ * each); in place. */
+ddl_result_t ddl_group_allreduce(ddl_comm_t comm, void* const* bufs, size_t count, ddl_dtype_t dtype,
+                                 ddl_op_t op, void* stream);
+/* sendbufs[r]: nranks*recvcount elements (not modified); recvbufs[r]: recvcount.
+ * Uses a library workspace of nranks * nranks * recvcount elements (grown on demand). */
+ddl_result_t ddl_group_reduce_scatter(ddl_comm_t comm, const void* const* sendbufs, void* const* recvbufs,
+                                      size_t recvcount, ddl_dtype_t dtype, ddl_op_t op, void* stream);
+/* sendbufs[r]: sendcount elements; recvbufs[r]: nranks*sendcount elements. */
+ddl_result_t ddl_group_allgather(ddl_comm_t comm, const void* const* sendbufs, void* const* recvbufs,
+                                 size_t sendcount, ddl_dtype_t dtype, void* stream);
+
+/* ------------------------------------------------------------------ local reduce (K5) */
+/* out[e] = scale * sum_{j<g} ins[j][e], folded in ascending j in fp32 (int32: wrapping,
+ * scale must be 1), one multiply by fl32(scale) (skipped when scale == 1), then the output
+ * cast (bf16: RNE).  ins: host array of g device pointers (g in [1, 64]); out may alias
+ * ins[0].  The 1-GPU HBM-roofline kernel of SURVEY.md 8(a) a8. */
+ddl_result_t ddl_local_reduce(const void* const* ins, int g, void* out, size_t count, ddl_dtype_t dtype,
+                              float scale, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDL_H */

@@ -1,0 +1,578 @@
+// ddl_device.cuh -- sm_100a kernels of libddl.
+//
+//   ddl_hier_kernel    one launch = one whole hierarchical collective: copy-in (staged),
+//                      RS phases d = live[0..L-1] (K1) with the fused 1/P + cast epilogue
+//                      in the last one (K3), AG phases d = live[L-1..0] (K2), copy-out,
+//                      separated by 2L+1 per-CTA device barriers (K4).
+//   ddl_oneshot_kernel small messages: every rank reads all P inputs, folds them in the
+//                      nested order of the dims (same F_dims as the hierarchy), 2 barriers.
+//   ddl_local_reduce_kernel  K5: out = s * sum_j in_j over local buffers (HBM roofline).
+//
+// Work split (a4 "per-CTA slices"): a block of q elements is cut into nctas slices; CTA c
+// handles slice c of every block in every phase, so CTA c only ever depends on CTA c of its
+// peers and the barriers are per CTA (no grid-wide sync).  In loopback mode the P virtual
+// ranks are gridDim.y and all P * nctas CTAs are co-resident (cooperative launch).
+//
+// Memory ordering (cross-GPU): all threads' stores -> __syncthreads -> one lane per peer
+// st.release.sys of the epoch into the peer's flag slot; waiters spin with ld.acquire.sys on
+// their local slot, then __syncthreads.  Data loads that may target memory another agent
+// wrote during this launch use ld.global.cg (L2 / remote, never a stale L1 line).
+// Numerics: __fadd_rn / __fmul_rn (never contracted into FMA), RNE bf16 cast, int32 adds in
+// uint32 (wrap); the fold order is ascending group coordinate.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "ddl_plan.h"
+
+namespace ddl {
+
+constexpr int kThreads = 512;
+constexpr int kMaxLocalIn = 64;
+
+enum Mode : int {
+  kCinAll = 1,    // copy cin[me] -> work[me] (all blocks, this CTA's slices) before the start
+  kCinOwn = 2,    // copy cin[me] (one block of q elems) -> work[me] block me
+  kRS = 4,
+  kAG = 8,
+  kCoutAll = 16,  // copy work[me] -> cout[me] (all blocks) after the AG phases
+};
+
+enum DType : int { kI32 = 0, kF32 = 1, kBF16 = 2 };
+enum Op : int { kSum = 0, kAvg = 1 };
+enum Err : int { kErrTimeout = 8 };
+
+struct KParams {
+  Topo t;
+  int rank;            // this process's rank (multi-process); loopback: me = blockIdx.y
+  int loopback;
+  int op;
+  int cmax;            // CTA stride of the flag slots
+  float scale;         // fl32(1/P) for avg
+  int skip_rank;       // test hook: this rank's CTAs return at once (-1: none)
+  uint64_t n;          // elements of the full vector
+  uint64_t q;          // block elements
+  uint64_t slice;      // elements per CTA slice (hier: of a block; one-shot: of the vector)
+  uint64_t timeout_ns;
+  int* err;            // sticky device error word (local)
+  uint32_t* flags[kMaxRanks];   // each rank's flag region (peer-mapped); [cmax epochs][slots][cmax][P]
+  const void* in[kMaxRanks];    // where RS phase live[0] (and the one-shot) reads each rank's input
+  void* work[kMaxRanks];        // each rank's working buffer (partials, gathered blocks)
+  void* out[kMaxRanks];         // last RS phase / one-shot destination of each rank (block offsets apply)
+  const void* cin[kMaxRanks];   // copy-in source of each rank
+  void* cout[kMaxRanks];        // copy-out destination of each rank
+  int mode;
+};
+
+struct LRParams {
+  const void* in[kMaxLocalIn];
+  void* out;
+  uint64_t n;
+  int g;
+  float scale;
+};
+
+// ------------------------------------------------------------------------ element traits
+template <typename T> struct Tr;
+template <> struct Tr<int32_t> {  // int32: wrapping adds in uint32
+  using Acc = uint32_t;
+  static constexpr int W = 4;
+  __device__ static Acc to(uint32_t bits) { return bits; }
+  __device__ static uint32_t from(Acc a) { return a; }
+  __device__ static Acc add(Acc a, Acc b) { return a + b; }
+  __device__ static Acc mul(Acc a, float) { return a; }
+  __device__ static Acc round(Acc a) { return a; }
+};
+template <> struct Tr<float> {
+  using Acc = float;
+  static constexpr int W = 4;
+  __device__ static Acc to(uint32_t bits) { return __uint_as_float(bits); }
+  __device__ static uint32_t from(Acc a) { return __float_as_uint(a); }
+  __device__ static Acc add(Acc a, Acc b) { return __fadd_rn(a, b); }
+  __device__ static Acc mul(Acc a, float s) { return __fmul_rn(a, s); }
+  __device__ static Acc round(Acc a) { return a; }
+};
+template <> struct Tr<__nv_bfloat16> {  // bf16 bits in memory, fp32 accumulation
+  using Acc = float;
+  static constexpr int W = 8;
+  __device__ static Acc to(uint32_t bits16) { return __uint_as_float(bits16 << 16); }
+  __device__ static uint32_t from(Acc a) {
+    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a));
+  }
+  __device__ static Acc add(Acc a, Acc b) { return __fadd_rn(a, b); }
+  __device__ static Acc mul(Acc a, float s) { return __fmul_rn(a, s); }
+  __device__ static Acc round(Acc a) { return to(from(a)); }  // bf16 phase-boundary rounding
+};
+
+// Unpack / pack one 16-byte vector (W elements).
+template <typename T>
+__device__ __forceinline__ void unpack(const uint4& r, typename Tr<T>::Acc* a) {
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  if constexpr (Tr<T>::W == 8) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[2 * i] = Tr<T>::to(w[i] & 0xFFFFu);
+      a[2 * i + 1] = Tr<T>::to(w[i] >> 16);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = Tr<T>::to(w[i]);
+  }
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack(const typename Tr<T>::Acc* a) {
+  uint32_t w[4];
+  if constexpr (Tr<T>::W == 8) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = Tr<T>::from(a[2 * i]) | (Tr<T>::from(a[2 * i + 1]) << 16);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = Tr<T>::from(a[i]);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t ld_elem(const char* p) {
+  if constexpr (sizeof(T) == 2) return (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(p));
+  else return __ldcg(reinterpret_cast<const unsigned int*>(p));
+}
+template <typename T>
+__device__ __forceinline__ void st_elem(char* p, uint32_t v) {
+  if constexpr (sizeof(T) == 2) *reinterpret_cast<unsigned short*>(p) = (unsigned short)v;
+  else *reinterpret_cast<unsigned int*>(p) = v;
+}
+__device__ __forceinline__ uint4 ld_vec(const char* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
+__device__ __forceinline__ void st_vec(char* p, const uint4& v) { *reinterpret_cast<uint4*>(p) = v; }
+
+// ------------------------------------------------------------------------ device barrier (K4)
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t* flag_slot(const KParams& p, uint32_t* base, int slot, int cta, int src) {
+  return base + p.cmax + ((size_t)slot * p.cmax + cta) * p.t.P + src;
+}
+
+// Barrier `slot` of CTA blockIdx.x of rank `me` with `np` peers given by peer(l).
+// Returns false (after recording DDL_ERR_TIMEOUT) if a peer did not arrive in time.
+template <typename PeerFn>
+__device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int np, uint32_t epoch, PeerFn peer) {
+  __syncthreads();  // every thread's stores of the previous phase precede the release below
+  int fail = 0;
+  if (threadIdx.x < np) {
+    const int m = peer(threadIdx.x);
+    st_release_sys(flag_slot(p, p.flags[m], slot, blockIdx.x, me), epoch);
+    const uint32_t* f = flag_slot(p, p.flags[me], slot, blockIdx.x, m);
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
+    while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
+      if ((++spins & 1023u) == 0) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > p.timeout_ns) {
+          atomicExch(p.err, kErrTimeout);
+          fail = 1;
+          break;
+        }
+      }
+    }
+  }
+  return __syncthreads_or(fail) == 0;
+}
+
+__device__ __forceinline__ uint32_t next_epoch(const KParams& p, int me) {
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) {
+    uint32_t* ep = p.flags[me] + blockIdx.x;  // this CTA's call counter, local memory
+    const uint32_t e = *ep + 1;
+    *ep = e;
+    s_epoch = e;
+  }
+  __syncthreads();
+  return s_epoch;
+}
+
+// ------------------------------------------------------------------------ block/slice helpers
+// CTA c handles, for every block b of a phase's block set, the elements
+// [b*q + c*slice, b*q + min((c+1)*slice, q)) clipped to n.  The part that is a whole number
+// of W-wide vectors goes through the 16-byte path; a ragged remainder (only where the
+// slice is cut by n) goes element by element.
+struct Span {
+  uint64_t e0;    // first element of this CTA's slice of the block
+  uint32_t nvec;  // full W-wide vectors
+  uint32_t rem;   // trailing elements after them (< W)
+};
+
+template <int W>
+__device__ __forceinline__ Span slice_span(const KParams& p, int b) {
+  Span s{0, 0, 0};
+  const uint64_t cbase = (uint64_t)blockIdx.x * p.slice;
+  if (cbase >= p.q) return s;
+  const uint64_t e0 = (uint64_t)b * p.q + cbase;
+  if (e0 >= p.n) return s;
+  uint64_t len = p.q - cbase < p.slice ? p.q - cbase : p.slice;
+  if (len > p.n - e0) len = p.n - e0;
+  s.e0 = e0;
+  s.nvec = (uint32_t)(len / W);
+  s.rem = (uint32_t)(len - (uint64_t)s.nvec * W);
+  return s;
+}
+
+// ------------------------------------------------------------------------ copies
+// Copy this CTA's slice of block b from src to dst (same element offsets; the source may
+// be shifted by src_shift elements, for the allgather copy-in of a one-block send buffer).
+template <typename T, bool VEC>
+__device__ __forceinline__ void copy_block(const KParams& p, const char* src, char* dst, int b,
+                                           int64_t src_shift) {
+  constexpr int W = VEC ? Tr<T>::W : 1;
+  constexpr int U = 8;
+  const Span s = slice_span<W>(p, b);
+  const char* ps = src + ((int64_t)s.e0 - src_shift) * (int64_t)sizeof(T);
+  char* pd = dst + s.e0 * sizeof(T);
+  for (uint32_t j0 = threadIdx.x; j0 < s.nvec; j0 += U * blockDim.x) {
+    uint4 v[U];
+    uint32_t e1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = j0 + u * blockDim.x;
+      if (j < s.nvec) {
+        if constexpr (VEC) v[u] = ld_vec(ps + (size_t)j * 16);
+        else e1[u] = ld_elem<T>(ps + (size_t)j * sizeof(T));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = j0 + u * blockDim.x;
+      if (j < s.nvec) {
+        if constexpr (VEC) st_vec(pd + (size_t)j * 16, v[u]);
+        else st_elem<T>(pd + (size_t)j * sizeof(T), e1[u]);
+      }
+    }
+  }
+  if (threadIdx.x < s.rem) {
+    const size_t o = ((size_t)s.nvec * W + threadIdx.x) * sizeof(T);
+    st_elem<T>(pd + o, ld_elem<T>(ps + o));
+  }
+}
+
+// ------------------------------------------------------------------------ RS phase (K1 + K3)
+// For each block b in A_{d+1}(me):  y = ((x_{m_0} + x_{m_1}) + ...) + x_{m_{g-1}}  (ascending
+// coordinate v of the group-d member), [ * fl32(1/P) in the last phase for avg ], cast, store.
+// G > 0: group size known at compile time (all loads of an item issued together);
+// G == 0: any g, loads issued in chunks of 8 members.
+template <typename T, bool VEC, int G>
+__device__ __forceinline__ void rs_phase(const KParams& p, int me, int d, bool first, bool last) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = VEC ? Tr<T>::W : 1;
+  constexpr int NA = W;
+  constexpr int GC = G > 0 ? G : 8;
+  constexpr int U = G > 0 ? (4 / G > 0 ? 4 / G : 1) : 1;  // <= 4 loads in flight per thread (no spills at 128 regs)
+  constexpr int ES = VEC ? 16 : (int)sizeof(T);
+  const Topo& t = p.t;
+  const int g = G > 0 ? G : t.g[d];
+  const bool do_scale = last && p.op == kAvg;
+  const int nb = nblocks(t, d + 1);
+  const void* const* srcs = first ? p.in : (const void* const*)p.work;
+  char* dstbase = static_cast<char*>(last ? p.out[me] : p.work[me]);
+  int mem[GC];
+  if constexpr (G > 0) {
+#pragma unroll
+    for (int v = 0; v < G; ++v) mem[v] = member(t, me, d, v);
+  }
+
+  for (int bi = 0; bi < nb; ++bi) {
+    const int b = block_of(t, me, d + 1, bi);
+    const Span s = slice_span<W>(p, b);
+    const size_t boff = s.e0 * sizeof(T);
+    char* pd = dstbase + boff;
+    for (uint32_t j0 = threadIdx.x; j0 < s.nvec; j0 += U * blockDim.x) {
+      A acc[U][NA];
+      for (int v0 = 0; v0 < g; v0 += GC) {
+        if constexpr (G == 0) {
+#pragma unroll
+          for (int v = 0; v < GC; ++v) mem[v] = v0 + v < g ? member(t, me, d, v0 + v) : me;
+        }
+        uint4 raw[U][GC];
+        uint32_t raw1[U][GC];
+#pragma unroll
+        for (int v = 0; v < GC; ++v) {
+          if (G == 0 && v0 + v >= g) break;
+          const char* ps = static_cast<const char*>(srcs[mem[v]]) + boff;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t j = j0 + u * blockDim.x;
+            if (j < s.nvec) {
+              if constexpr (VEC) raw[u][v] = ld_vec(ps + (size_t)j * ES);
+              else raw1[u][v] = ld_elem<T>(ps + (size_t)j * ES);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int v = 0; v < GC; ++v) {
+            if (G == 0 && v0 + v >= g) break;
+            A x[NA];
+            if constexpr (VEC) unpack<T>(raw[u][v], x);
+            else x[0] = Tr<T>::to(raw1[u][v]);
+#pragma unroll
+            for (int i = 0; i < NA; ++i) acc[u][i] = (v0 + v == 0) ? x[i] : Tr<T>::add(acc[u][i], x[i]);
+          }
+          if (v0 + GC >= g) {  // fold complete: epilogue (K3) and store
+            const uint32_t j = j0 + u * blockDim.x;
+            if (j < s.nvec) {
+              if (do_scale) {
+#pragma unroll
+                for (int i = 0; i < NA; ++i) acc[u][i] = Tr<T>::mul(acc[u][i], p.scale);
+              }
+              if constexpr (VEC) st_vec(pd + (size_t)j * ES, pack<T>(acc[u]));
+              else st_elem<T>(pd + (size_t)j * ES, Tr<T>::from(acc[u][0]));
+            }
+          }
+        }
+      }
+    }
+    if (threadIdx.x < s.rem) {  // ragged end of the vector, element by element
+      const size_t o = boff + ((size_t)s.nvec * W + threadIdx.x) * sizeof(T);
+      A a = 0;
+      for (int v = 0; v < g; ++v) {
+        const A x = Tr<T>::to(ld_elem<T>(static_cast<const char*>(srcs[member(t, me, d, v)]) + o));
+        a = v == 0 ? x : Tr<T>::add(a, x);
+      }
+      if (do_scale) a = Tr<T>::mul(a, p.scale);
+      st_elem<T>(dstbase + o, Tr<T>::from(a));
+    }
+  }
+}
+
+template <typename T, bool VEC>
+__device__ __forceinline__ void rs_dispatch(const KParams& p, int me, int d, bool first, bool last) {
+  switch (p.t.g[d]) {
+    case 2: rs_phase<T, VEC, 2>(p, me, d, first, last); break;
+    case 3: rs_phase<T, VEC, 3>(p, me, d, first, last); break;
+    case 4: rs_phase<T, VEC, 4>(p, me, d, first, last); break;
+    case 8: rs_phase<T, VEC, 8>(p, me, d, first, last); break;
+    default: rs_phase<T, VEC, 0>(p, me, d, first, last); break;
+  }
+}
+
+// ------------------------------------------------------------------------ AG phase (K2)
+// For every group-d peer m_v (v != c_d(me)) and every block b in A_{d+1}(m_v): copy this
+// CTA's slice of block b from work[m_v] to work[me].  Pure bit copy.
+template <typename T, bool VEC>
+__device__ __forceinline__ void ag_phase(const KParams& p, int me, int d) {
+  const Topo& t = p.t;
+  const int c = coord(t, me, d);
+  const int nb = nblocks(t, d + 1);
+  for (int v = 0; v < t.g[d]; ++v) {
+    if (v == c) continue;
+    const int m = member(t, me, d, v);
+    for (int bi = 0; bi < nb; ++bi)
+      copy_block<T, VEC>(p, static_cast<const char*>(p.work[m]), static_cast<char*>(p.work[me]),
+                         block_of(t, m, d + 1, bi), 0);
+  }
+}
+
+// ------------------------------------------------------------------------ the hierarchical kernel
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads, 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
+  const int me = p.loopback ? (int)blockIdx.y : p.rank;
+  const uint32_t e = next_epoch(p, me);
+  if (me == p.skip_rank) return;
+  const Topo& t = p.t;
+  const int L = t.nlive;
+  const int me_ = me;
+  auto group_peer = [&](int j) { return [&p, me_, j](int l) { return barrier_peer(p.t, me_, j, l); }; };
+
+  if (p.mode & kCinAll)
+    for (int b = 0; b < t.P; ++b)
+      copy_block<T, VEC>(p, static_cast<const char*>(p.cin[me]), static_cast<char*>(p.work[me]), b, 0);
+  if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T))
+    copy_block<T, VEC>(p, static_cast<const char*>(p.cin[me]), static_cast<char*>(p.work[me]), me,
+                       (int64_t)me * (int64_t)p.q);
+  if (p.mode & kRS) {
+    for (int j = 0; j < L; ++j) {
+      if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
+      rs_dispatch<T, VEC>(p, me, t.live[j], j == 0, j == L - 1);
+    }
+  }
+  if (p.mode & kAG) {
+    for (int jj = 0; jj < L; ++jj) {
+      const int j = L + jj;
+      if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
+      ag_phase<T, VEC>(p, me, t.live[L - 1 - jj]);
+    }
+  }
+  if (p.mode & kCoutAll)
+    for (int b = 0; b < t.P; ++b)
+      copy_block<T, VEC>(p, static_cast<const char*>(p.work[me]), static_cast<char*>(p.cout[me]), b, 0);
+  if (L > 0) dbarrier(p, me, 2 * L, barrier_npeers(t, 2 * L), e, group_peer(2 * L));
+}
+
+// ------------------------------------------------------------------------ one-shot (a9)
+// Every rank reads slice c of all P inputs, folds them in the nested order of the live dims
+// (level j folds consecutive groups of g_{live[j]} values, rounding at each level like a
+// phase boundary, the avg multiply fused into the last level), waits until every rank has
+// finished reading, then writes its result.  K = number of live dims (templated so the
+// level accumulators stay in registers).
+
+// Feed value x (of rank r, ascending) into the level accumulators; when the last level
+// completes, its (scaled, rounded) value is written to res.
+template <typename T, int K, int NA>
+__device__ __forceinline__ void nested_feed(const KParams& p, const int* gl, const int* Gl, int r,
+                                            typename Tr<T>::Acc (*lvl)[NA], typename Tr<T>::Acc* x,
+                                            typename Tr<T>::Acc* res) {
+  using A = typename Tr<T>::Acc;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int pos = (r / Gl[j]) % gl[j];
+#pragma unroll
+    for (int k = 0; k < NA; ++k) lvl[j][k] = pos == 0 ? x[k] : Tr<T>::add(lvl[j][k], x[k]);
+    if (pos != gl[j] - 1) break;  // group of level j not complete yet
+    const bool top = (j == K - 1);
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+      A y = lvl[j][k];
+      if (top && p.op == kAvg) y = Tr<T>::mul(y, p.scale);
+      x[k] = Tr<T>::round(y);
+      if (top) res[k] = x[k];
+    }
+  }
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_constant__ KParams p) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = Tr<T>::W;
+  constexpr int CH = 8;
+  const int me = p.loopback ? (int)blockIdx.y : p.rank;
+  const uint32_t e = next_epoch(p, me);
+  if (me == p.skip_rank) return;
+  const Topo& t = p.t;
+  const int P = t.P;
+  int gl[K], Gl[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    gl[j] = t.g[t.live[j]];
+    Gl[j] = t.G[t.live[j]];
+  }
+  const uint64_t lo = (uint64_t)blockIdx.x * p.slice;
+  const uint64_t eoff = lo + (uint64_t)threadIdx.x * W;   // one vector per thread
+  const uint64_t hi = lo + p.slice < p.n ? lo + p.slice : p.n;
+  const bool full = eoff + W <= hi;
+  const int ntail = (!full && eoff < hi) ? (int)(hi - eoff) : 0;
+  auto all = [me](int l) { return all_peer(me, l); };
+
+  if (p.mode & kCinAll) {  // staged: publish this CTA's slice of my input
+    const char* s = static_cast<const char*>(p.cin[me]);
+    char* w = static_cast<char*>(p.work[me]);
+    if (full) st_vec(w + eoff * sizeof(T), ld_vec(s + eoff * sizeof(T)));
+    for (int i = 0; i < ntail; ++i)
+      st_elem<T>(w + (eoff + i) * sizeof(T), ld_elem<T>(s + (eoff + i) * sizeof(T)));
+  }
+  if (!dbarrier(p, me, 0, P - 1, e, all)) return;
+
+  A res[W];
+  if (full) {
+    A lvl[K][W];
+    for (int r0 = 0; r0 < P; r0 += CH) {
+      uint4 raw[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        if (r0 + i >= P) break;
+        raw[i] = ld_vec(static_cast<const char*>(p.in[r0 + i]) + eoff * sizeof(T));
+      }
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        if (r0 + i >= P) break;
+        A x[W];
+        unpack<T>(raw[i], x);
+        nested_feed<T, K, W>(p, gl, Gl, r0 + i, lvl, x, res);
+      }
+    }
+  } else {
+    for (int k = 0; k < ntail; ++k) {  // ragged end of the vector, one element at a time
+      A lvl1[K][1];
+      A r1[1];
+      for (int r = 0; r < P; ++r) {
+        A x[1] = {Tr<T>::to(ld_elem<T>(static_cast<const char*>(p.in[r]) + (eoff + k) * sizeof(T)))};
+        nested_feed<T, K, 1>(p, gl, Gl, r, lvl1, x, r1);
+      }
+      res[k] = r1[0];
+    }
+  }
+  if (!dbarrier(p, me, 1, P - 1, e, all)) return;
+  char* o = static_cast<char*>(p.out[me]);
+  if (full) st_vec(o + eoff * sizeof(T), pack<T>(res));
+  for (int k = 0; k < ntail; ++k) st_elem<T>(o + (eoff + k) * sizeof(T), Tr<T>::from(res[k]));
+  if (p.mode & kCoutAll) {  // (unused: the staged one-shot writes the user buffer directly)
+  }
+}
+
+// ------------------------------------------------------------------------ K5 local reduce
+// out = s * sum_{j<g} in_j, ascending j.  Grid-stride over 16-byte vectors, up to 8 input
+// loads in flight per thread, streaming cache hints (every byte is touched once).
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads, 2) ddl_local_reduce_kernel(const __grid_constant__ LRParams p) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = VEC ? Tr<T>::W : 1;
+  constexpr int CH = 8;
+  const uint64_t nitems = p.n / W;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const bool do_scale = p.scale != 1.0f;
+  for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < nitems; it += stride) {
+    A acc[W];
+    for (int j0 = 0; j0 < p.g; j0 += CH) {
+      uint4 raw[CH];
+      uint32_t raw1[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        if (j0 + j >= p.g) break;
+        const char* ps = static_cast<const char*>(p.in[j0 + j]) + it * W * sizeof(T);
+        if constexpr (VEC) raw[j] = __ldcs(reinterpret_cast<const uint4*>(ps));
+        else raw1[j] = ld_elem<T>(ps);
+      }
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        if (j0 + j >= p.g) break;
+        A x[W];
+        if constexpr (VEC) unpack<T>(raw[j], x);
+        else x[0] = Tr<T>::to(raw1[j]);
+#pragma unroll
+        for (int i = 0; i < W; ++i) acc[i] = (j0 + j == 0) ? x[i] : Tr<T>::add(acc[i], x[i]);
+      }
+    }
+    if (do_scale) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) acc[i] = Tr<T>::mul(acc[i], p.scale);
+    }
+    char* pd = static_cast<char*>(p.out) + it * W * sizeof(T);
+    if constexpr (VEC) __stcs(reinterpret_cast<uint4*>(pd), pack<T>(acc));
+    else st_elem<T>(pd, Tr<T>::from(acc[0]));
+  }
+  if constexpr (VEC) {  // the last n % W elements
+    if (blockIdx.x == 0) {
+      const uint64_t e = nitems * W + threadIdx.x;
+      if (e < p.n) {
+        A a = Tr<T>::to(ld_elem<T>(static_cast<const char*>(p.in[0]) + e * sizeof(T)));
+        for (int j = 1; j < p.g; ++j)
+          a = Tr<T>::add(a, Tr<T>::to(ld_elem<T>(static_cast<const char*>(p.in[j]) + e * sizeof(T))));
+        if (do_scale) a = Tr<T>::mul(a, p.scale);
+        st_elem<T>(static_cast<char*>(p.out) + e * sizeof(T), Tr<T>::from(a));
+      }
+    }
+  }
+}
+
+}  // namespace ddl

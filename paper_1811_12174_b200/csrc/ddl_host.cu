@@ -1,0 +1,769 @@
+// ddl_host.cu -- libddl's C ABI (include/ddl.h): communicator lifecycle, cudaIpc peer
+// mapping, the per-call planner (block size, CTA slices, algorithm choice) and the kernel
+// launches.  See DESIGN.md for the design and the paper citations.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <unordered_map>
+
+#include "ddl.h"
+#include "ddl_device.cuh"
+#include "ddl_plan.h"
+
+using namespace ddl;
+
+static_assert(DDL_MAX_RANKS == kMaxRanks, "header / planner rank limit");
+static_assert(DDL_MAX_DIMS == kMaxDims, "header / planner dims limit");
+
+namespace {
+
+constexpr uint32_t kMagic = 0xDD1A11EDu;
+constexpr int kNumSlots = 2 * kMaxDims + 1;
+
+thread_local std::string g_last_error;
+
+ddl_result_t cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  if (std::getenv("DDL_DEBUG")) std::fprintf(stderr, "[ddl] %s\n", g_last_error.c_str());
+  return DDL_ERR_CUDA;
+}
+#define DDL_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+size_t env_size(const char* name, size_t dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return (size_t)std::strtoull(v, nullptr, 10);
+}
+
+int elem_size(ddl_dtype_t dt) { return dt == DDL_BFLOAT16 ? 2 : 4; }
+bool valid_dtype(int dt) { return dt == DDL_INT32 || dt == DDL_FLOAT32 || dt == DDL_BFLOAT16; }
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+struct Handle {  // exported per rank, all-gathered by the caller
+  uint32_t magic;
+  int32_t rank, nranks, ndims;
+  int32_t dims[kMaxDims];
+  int32_t cmax;
+  int32_t pad;
+  uint64_t flags_bytes, max_bytes, alloc_bytes;
+  char pci[32];
+  cudaIpcMemHandle_t ipc;
+};
+
+}  // namespace
+
+struct ddl_comm {
+  bool loopback = false;
+  int rank = 0;
+  int P = 1;
+  int ndims = 1;
+  int dims[kMaxDims] = {1};
+  Topo topo{};
+  int device = 0;
+  int num_sms = 148;
+  int cmax = 0;
+  size_t flags_bytes = 0;  // per rank
+  size_t max_bytes = 0;
+  // multi-process: [flags | symmetric buffer | staging], one allocation, one IPC handle
+  char* alloc = nullptr;
+  size_t alloc_bytes = 0;
+  char* peer_base[kMaxRanks] = {};
+  bool peer_mapped[kMaxRanks] = {};
+  bool connected = false;
+  // loopback: P flag regions + RS workspace
+  char* lb_flags = nullptr;
+  char* lb_ws = nullptr;
+  size_t lb_ws_bytes = 0;  // per virtual rank
+  int* err = nullptr;      // sticky device error
+  ddl_algo_t algo = DDL_ALGO_AUTO;
+  size_t oneshot_max = 256 << 10;
+  size_t min_slice_bytes = 16 << 10;
+  int ctas_limit = 0;  // 0 = occupancy bound
+  uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
+  int skip_rank = -1;
+
+  uint32_t* flags_of(int r) const {
+    if (loopback) return reinterpret_cast<uint32_t*>(lb_flags + (size_t)r * flags_bytes);
+    return reinterpret_cast<uint32_t*>(r == rank ? alloc : peer_base[r]);
+  }
+  char* sym_of(int r) const { return (r == rank ? alloc : peer_base[r]) + flags_bytes; }
+  char* stage_of(int r) const { return (r == rank ? alloc : peer_base[r]) + flags_bytes + max_bytes; }
+};
+
+namespace {
+
+// Resident CTAs (kThreads each) per SM for a kernel, cached.
+int blocks_per_sm(const void* fn) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) nb = 1;
+  if (nb < 1) nb = 1;
+  cache[fn] = nb;
+  return nb;
+}
+
+void apply_env(ddl_comm* c) {
+  c->timeout_ns = env_size("DDL_TIMEOUT_MS", 10000) * 1000000ull;
+  c->oneshot_max = env_size("DDL_ONESHOT_MAX_BYTES", c->oneshot_max);
+  c->min_slice_bytes = env_size("DDL_MIN_SLICE_BYTES", c->min_slice_bytes);
+  c->ctas_limit = (int)env_size("DDL_CTAS", 0);
+  if (const char* a = std::getenv("DDL_ALGO")) {
+    if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
+    else if (!std::strcmp(a, "oneshot")) c->algo = DDL_ALGO_ONESHOT;
+    else c->algo = DDL_ALGO_AUTO;
+  }
+}
+
+ddl_result_t common_init(ddl_comm* c, int nranks, const int* dims, int ndims, int dev) {
+  if (!dims) return DDL_ERR_INVALID_ARGUMENT;
+  if (nranks > kMaxRanks) return DDL_ERR_UNSUPPORTED;
+  if (make_topo(&c->topo, nranks, dims, ndims)) return DDL_ERR_BAD_DIMS;
+  c->P = nranks;
+  c->ndims = ndims;
+  for (int d = 0; d < ndims; ++d) c->dims[d] = dims[d];
+  c->device = dev;
+  DDL_CUDA(cudaSetDevice(dev));
+  DDL_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  c->cmax = c->num_sms * 4;
+  const size_t words = (size_t)c->cmax * (1 + (size_t)kNumSlots * nranks);
+  c->flags_bytes = (words * 4 + 65535) / 65536 * 65536;
+  apply_env(c);
+  return DDL_SUCCESS;
+}
+
+// ---------------------------------------------------------------- per-call plan
+struct Plan {
+  uint64_t q = 0;
+  uint64_t slice = 0;
+  int nctas = 0;
+  bool vec = true;
+  bool oneshot = false;
+};
+
+template <typename T>
+const void* hier_fn(bool vec) {
+  return vec ? (const void*)ddl_hier_kernel<T, true> : (const void*)ddl_hier_kernel<T, false>;
+}
+template <typename T>
+const void* oneshot_fn(int K) {
+  switch (K) {
+    case 1: return (const void*)ddl_oneshot_kernel<T, 1>;
+    case 2: return (const void*)ddl_oneshot_kernel<T, 2>;
+    case 3: return (const void*)ddl_oneshot_kernel<T, 3>;
+    case 4: return (const void*)ddl_oneshot_kernel<T, 4>;
+    default: return nullptr;
+  }
+}
+const void* hier_fn_dt(ddl_dtype_t dt, bool vec) {
+  if (dt == DDL_INT32) return hier_fn<int32_t>(vec);
+  if (dt == DDL_FLOAT32) return hier_fn<float>(vec);
+  return hier_fn<__nv_bfloat16>(vec);
+}
+const void* oneshot_fn_dt(ddl_dtype_t dt, int K) {
+  if (dt == DDL_INT32) return oneshot_fn<int32_t>(K);
+  if (dt == DDL_FLOAT32) return oneshot_fn<float>(K);
+  return oneshot_fn<__nv_bfloat16>(K);
+}
+
+// CTAs per rank that may be resident at once (loopback: all P ranks share the GPU).
+int cap_per_rank(const ddl_comm* c, const void* fn) {
+  int cap = blocks_per_sm(fn) * c->num_sms;
+  if (c->loopback) cap /= c->P;
+  if (c->ctas_limit > 0 && c->ctas_limit < cap) cap = c->ctas_limit;
+  if (cap > c->cmax) cap = c->cmax;
+  return cap < 1 ? 1 : cap;
+}
+
+Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool vec) {
+  Plan pl;
+  pl.q = q;
+  pl.vec = vec;
+  const int w = elem_size(dt);
+  const uint64_t W = vec ? 16 / w : 1;
+  const int cap = cap_per_rank(c, hier_fn_dt(dt, vec));
+  uint64_t want = (q * w + c->min_slice_bytes - 1) / c->min_slice_bytes;
+  if (want < 1) want = 1;
+  if (want > (uint64_t)cap) want = cap;
+  uint64_t slice = (q + want - 1) / want;
+  slice = (slice + W - 1) / W * W;
+  if (slice == 0) slice = W;
+  pl.slice = slice;
+  pl.nctas = (int)((q + slice - 1) / slice);
+  if (pl.nctas < 1) pl.nctas = 1;
+  (void)n;
+  return pl;
+}
+
+bool plan_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
+  const int K = c->topo.nlive;
+  const void* fn = oneshot_fn_dt(dt, K);
+  if (!fn) return false;
+  const uint64_t per_cta = (uint64_t)kThreads * (16 / elem_size(dt));
+  const uint64_t ctas = (n + per_cta - 1) / per_cta;
+  if (ctas > (uint64_t)cap_per_rank(c, fn)) return false;
+  pl->oneshot = true;
+  pl->vec = true;
+  pl->q = 0;
+  pl->slice = per_cta;
+  pl->nctas = (int)ctas;
+  return true;
+}
+
+bool use_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
+  if (c->P < 2 || c->algo == DDL_ALGO_HIER) return false;
+  if (c->algo == DDL_ALGO_AUTO && n * (uint64_t)elem_size(dt) > c->oneshot_max) return false;
+  return plan_oneshot(c, n, dt, pl);
+}
+
+KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
+  KParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.t = c->topo;
+  p.rank = c->rank;
+  p.loopback = c->loopback ? 1 : 0;
+  p.op = op;
+  p.cmax = c->cmax;
+  p.scale = 1.0f / (float)c->P;  // fl32(1/P)
+  p.skip_rank = c->skip_rank;
+  p.n = n;
+  p.timeout_ns = c->timeout_ns;
+  p.err = c->err;
+  for (int r = 0; r < c->P; ++r) p.flags[r] = c->flags_of(r);
+  return p;
+}
+
+ddl_result_t launch(const ddl_comm* c, const KParams& p, const Plan& pl, ddl_dtype_t dt, void* stream) {
+  const void* fn = pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive) : hier_fn_dt(dt, pl.vec);
+  if (!fn) return DDL_ERR_UNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  void* args[] = {const_cast<KParams*>(&p)};
+  if (std::getenv("DDL_DEBUG"))
+    std::fprintf(stderr, "[ddl] %s n=%llu q=%llu slice=%llu ctas=%d vec=%d mode=%d P=%d loopback=%d\n",
+                 pl.oneshot ? "oneshot" : "hier", (unsigned long long)p.n, (unsigned long long)p.q,
+                 (unsigned long long)p.slice, pl.nctas, (int)pl.vec, p.mode, c->P, (int)c->loopback);
+  if (c->loopback) {
+    DDL_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pl.nctas, c->P), dim3(kThreads), args, 0, s));
+  } else {
+    DDL_CUDA(cudaLaunchKernel(fn, dim3(pl.nctas), dim3(kThreads), args, 0, s));
+  }
+  return DDL_SUCCESS;
+}
+
+ddl_result_t check_common(const ddl_comm* c, ddl_dtype_t dt, ddl_op_t op) {
+  if (!c) return DDL_ERR_INVALID_ARGUMENT;
+  if (!valid_dtype(dt) || (op != DDL_SUM && op != DDL_AVG)) return DDL_ERR_INVALID_ARGUMENT;
+  if (dt == DDL_INT32 && op == DDL_AVG) return DDL_ERR_UNSUPPORTED;
+  if (!c->loopback && !c->connected && c->P > 1) return DDL_ERR_NOT_CONNECTED;
+  return DDL_SUCCESS;
+}
+
+// Local copy (P = 1 reduce-scatter / allgather) through the local-reduce kernel.
+ddl_result_t local_copy(const void* src, void* dst, size_t count, ddl_dtype_t dt, void* stream) {
+  if (src == dst || count == 0) return DDL_SUCCESS;
+  const void* ins[1] = {src};
+  return ddl_local_reduce(ins, 1, dst, count, dt, 1.0f, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ddl_version(void) { return 100; }
+
+const char* ddl_result_string(ddl_result_t r) {
+  switch (r) {
+    case DDL_SUCCESS: return "success";
+    case DDL_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case DDL_ERR_BAD_DIMS: return "bad dims (product != nranks, g < 1 or too many dims)";
+    case DDL_ERR_UNSUPPORTED: return "unsupported";
+    case DDL_ERR_CUDA: return "CUDA error";
+    case DDL_ERR_NO_PEER_ACCESS: return "no peer access";
+    case DDL_ERR_NOT_CONNECTED: return "not connected";
+    case DDL_ERR_TOO_LARGE: return "message larger than the workspace";
+    case DDL_ERR_TIMEOUT: return "device barrier timeout";
+    case DDL_ERR_MISMATCH: return "handle mismatch between ranks";
+  }
+  return "unknown";
+}
+
+const char* ddl_last_error_string(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------ planner queries
+ddl_result_t ddl_check_dims(int nranks, const int* dims, int ndims) {
+  if (!dims) return DDL_ERR_INVALID_ARGUMENT;
+  Topo t;
+  return make_topo(&t, nranks, dims, ndims) ? DDL_ERR_BAD_DIMS : DDL_SUCCESS;
+}
+
+size_t ddl_block_elems(size_t count, int nranks, ddl_dtype_t dtype) {
+  if (nranks < 1 || !valid_dtype(dtype)) return 0;
+  return (size_t)block_elems(count, nranks, elem_size(dtype));
+}
+
+ddl_result_t ddl_plan_group(int nranks, const int* dims, int ndims, int rank, int d, int* members_out) {
+  Topo t;
+  if (!dims || !members_out) return DDL_ERR_INVALID_ARGUMENT;
+  if (make_topo(&t, nranks, dims, ndims)) return DDL_ERR_BAD_DIMS;
+  if (rank < 0 || rank >= nranks || d < 0 || d >= ndims) return DDL_ERR_INVALID_ARGUMENT;
+  for (int v = 0; v < t.g[d]; ++v) members_out[v] = member(t, rank, d, v);
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_plan_blocks(int nranks, const int* dims, int ndims, int rank, int d, int* blocks_out,
+                             int* nblocks_out) {
+  Topo t;
+  if (!dims || !blocks_out || !nblocks_out) return DDL_ERR_INVALID_ARGUMENT;
+  if (make_topo(&t, nranks, dims, ndims)) return DDL_ERR_BAD_DIMS;
+  if (rank < 0 || rank >= nranks || d < 0 || d > ndims) return DDL_ERR_INVALID_ARGUMENT;
+  *nblocks_out = nblocks(t, d);
+  for (int i = 0; i < *nblocks_out; ++i) blocks_out[i] = block_of(t, rank, d, i);
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_plan_barriers(int nranks, const int* dims, int ndims, int rank, int* peers_out,
+                               int* counts_out, int* nbarriers_out) {
+  Topo t;
+  if (!dims || !peers_out || !counts_out || !nbarriers_out) return DDL_ERR_INVALID_ARGUMENT;
+  if (make_topo(&t, nranks, dims, ndims)) return DDL_ERR_BAD_DIMS;
+  if (rank < 0 || rank >= nranks) return DDL_ERR_INVALID_ARGUMENT;
+  const int nb = t.nlive ? 2 * t.nlive + 1 : 0;
+  *nbarriers_out = nb;
+  for (int j = 0; j < nb; ++j) {
+    counts_out[j] = barrier_npeers(t, j);
+    for (int l = 0; l < counts_out[j]; ++l) peers_out[j * nranks + l] = barrier_peer(t, rank, j, l);
+  }
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_plan_traffic(size_t count, ddl_dtype_t dtype, int nranks, const int* dims, int ndims, int rank,
+                              uint64_t* rs_out, uint64_t* ag_out) {
+  Topo t;
+  if (!dims || !rs_out || !ag_out || !valid_dtype(dtype)) return DDL_ERR_INVALID_ARGUMENT;
+  if (make_topo(&t, nranks, dims, ndims)) return DDL_ERR_BAD_DIMS;
+  if (rank < 0 || rank >= nranks) return DDL_ERR_INVALID_ARGUMENT;
+  const int w = elem_size(dtype);
+  const uint64_t n = count, q = block_elems(count, nranks, w);
+  auto len = [&](int b) -> uint64_t {
+    const uint64_t lo = (uint64_t)b * q < n ? (uint64_t)b * q : n;
+    const uint64_t hi = (uint64_t)(b + 1) * q < n ? (uint64_t)(b + 1) * q : n;
+    return hi - lo;
+  };
+  for (int d = 0; d < ndims; ++d) {
+    rs_out[d] = ag_out[d] = 0;
+    if (t.g[d] == 1) continue;
+    for (int i = 0; i < nblocks(t, d + 1); ++i)
+      rs_out[d] += (uint64_t)(t.g[d] - 1) * len(block_of(t, rank, d + 1, i)) * w;
+    for (int v = 0; v < t.g[d]; ++v) {
+      const int m = member(t, rank, d, v);
+      if (m == rank) continue;
+      for (int i = 0; i < nblocks(t, d + 1); ++i) ag_out[d] += len(block_of(t, m, d + 1, i)) * w;
+    }
+  }
+  return DDL_SUCCESS;
+}
+
+// ------------------------------------------------------------------ multi-process comm
+ddl_result_t ddl_init(ddl_comm_t* comm, int rank, int nranks, const int* dims, int ndims, int cuda_device,
+                      size_t max_bytes) {
+  if (!comm || rank < 0 || rank >= nranks) return DDL_ERR_INVALID_ARGUMENT;
+  *comm = nullptr;
+  ddl_comm* c = new (std::nothrow) ddl_comm();
+  if (!c) return DDL_ERR_CUDA;
+  ddl_result_t r = common_init(c, nranks, dims, ndims, cuda_device);
+  if (r != DDL_SUCCESS) {
+    delete c;
+    return r;
+  }
+  c->rank = rank;
+  c->max_bytes = (max_bytes + 4095) / 4096 * 4096;
+  c->alloc_bytes = c->flags_bytes + 2 * c->max_bytes;
+  cudaError_t e = cudaMalloc(&c->alloc, c->alloc_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->alloc, 0, c->flags_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (c->alloc) cudaFree(c->alloc);
+    if (c->err) cudaFree(c->err);
+    delete c;
+    return cuda_fail(e, "ddl_init allocation");
+  }
+  c->connected = (nranks == 1);
+  *comm = c;
+  return DDL_SUCCESS;
+}
+
+size_t ddl_handle_size(void) { return sizeof(Handle); }
+
+ddl_result_t ddl_export_handle(ddl_comm_t c, void* out) {
+  if (!c || !out || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  Handle h;
+  std::memset(&h, 0, sizeof(h));
+  h.magic = kMagic;
+  h.rank = c->rank;
+  h.nranks = c->P;
+  h.ndims = c->ndims;
+  for (int d = 0; d < c->ndims; ++d) h.dims[d] = c->dims[d];
+  h.cmax = c->cmax;
+  h.flags_bytes = c->flags_bytes;
+  h.max_bytes = c->max_bytes;
+  h.alloc_bytes = c->alloc_bytes;
+  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_CUDA(cudaDeviceGetPCIBusId(h.pci, sizeof(h.pci), c->device));
+  DDL_CUDA(cudaIpcGetMemHandle(&h.ipc, c->alloc));
+  std::memcpy(out, &h, sizeof(h));
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_connect(ddl_comm_t c, const void* all_handles) {
+  if (!c || !all_handles || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  if (c->connected) return DDL_SUCCESS;
+  DDL_CUDA(cudaSetDevice(c->device));
+  const Handle* hs = static_cast<const Handle*>(all_handles);
+  for (int m = 0; m < c->P; ++m) {
+    const Handle& h = hs[m];
+    if (h.magic != kMagic || h.rank != m) return DDL_ERR_INVALID_ARGUMENT;
+    if (h.nranks != c->P || h.ndims != c->ndims || h.cmax != c->cmax || h.flags_bytes != c->flags_bytes ||
+        h.max_bytes != c->max_bytes)
+      return DDL_ERR_MISMATCH;
+    for (int d = 0; d < c->ndims; ++d)
+      if (h.dims[d] != c->dims[d]) return DDL_ERR_MISMATCH;
+  }
+  for (int m = 0; m < c->P; ++m) {
+    if (m == c->rank) continue;
+    const Handle& h = hs[m];
+    int pdev = -1;
+    if (cudaDeviceGetByPCIBusId(&pdev, h.pci) == cudaSuccess && pdev != c->device) {
+      int ok = 0;
+      DDL_CUDA(cudaDeviceCanAccessPeer(&ok, c->device, pdev));
+      if (!ok) return DDL_ERR_NO_PEER_ACCESS;
+    }
+    cudaGetLastError();
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h.ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    c->peer_base[m] = static_cast<char*>(ptr);
+    c->peer_mapped[m] = true;
+  }
+  c->connected = true;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_buffer(ddl_comm_t c, void** dev_ptr, size_t* bytes) {
+  if (!c || !dev_ptr || !bytes || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  *dev_ptr = c->alloc + c->flags_bytes;
+  *bytes = c->max_bytes;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_allreduce(ddl_comm_t c, void* buf, size_t count, ddl_dtype_t dt, ddl_op_t op, void* stream) {
+  ddl_result_t r = check_common(c, dt, op);
+  if (r != DDL_SUCCESS) return r;
+  if (c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  if (count == 0 || c->P == 1) return DDL_SUCCESS;
+  if (!buf || !aligned16(buf)) return DDL_ERR_INVALID_ARGUMENT;
+  const size_t bytes = count * elem_size(dt);
+  char* sym = c->alloc + c->flags_bytes;
+  const bool zero_copy = (char*)buf >= sym && (char*)buf + bytes <= sym + c->max_bytes;
+  if (!zero_copy && bytes > c->max_bytes) return DDL_ERR_TOO_LARGE;
+  DDL_CUDA(cudaSetDevice(c->device));
+  KParams p = base_params(c, count, op);
+  Plan pl;
+  const bool one = use_oneshot(c, count, dt, &pl);
+  if (!one) pl = plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true);
+  p.q = pl.q;
+  p.slice = pl.slice;
+  const size_t off = zero_copy ? (size_t)((char*)buf - sym) : 0;
+  for (int m = 0; m < c->P; ++m) {
+    char* base = zero_copy ? c->sym_of(m) + off : c->stage_of(m);
+    p.in[m] = base;
+    p.work[m] = base;
+    p.out[m] = base;
+  }
+  if (one) {
+    p.mode = zero_copy ? 0 : kCinAll;
+    p.cin[c->rank] = buf;
+    p.out[c->rank] = buf;
+  } else {
+    p.mode = kRS | kAG | (zero_copy ? 0 : (kCinAll | kCoutAll));
+    p.cin[c->rank] = buf;
+    p.cout[c->rank] = buf;
+  }
+  return launch(c, p, pl, dt, stream);
+}
+
+ddl_result_t ddl_reduce_scatter(ddl_comm_t c, const void* sendbuf, void* recvbuf, size_t recvcount, ddl_dtype_t dt,
+                                ddl_op_t op, void* stream) {
+  ddl_result_t r = check_common(c, dt, op);
+  if (r != DDL_SUCCESS) return r;
+  if (c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  if (recvcount == 0) return DDL_SUCCESS;
+  if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return DDL_ERR_INVALID_ARGUMENT;
+  const int w = elem_size(dt);
+  if (c->P == 1) return local_copy(sendbuf, recvbuf, recvcount, dt, stream);
+  const size_t n = recvcount * (size_t)c->P;
+  if (n * w > c->max_bytes) return DDL_ERR_TOO_LARGE;
+  DDL_CUDA(cudaSetDevice(c->device));
+  const bool vec = (recvcount * w) % 16 == 0;
+  Plan pl = plan_hier(c, n, recvcount, dt, vec);
+  KParams p = base_params(c, n, op);
+  p.q = pl.q;
+  p.slice = pl.slice;
+  for (int m = 0; m < c->P; ++m) {
+    p.in[m] = c->stage_of(m);
+    p.work[m] = c->stage_of(m);
+  }
+  p.cin[c->rank] = sendbuf;
+  p.out[c->rank] = static_cast<char*>(recvbuf) - (ptrdiff_t)c->rank * (ptrdiff_t)(recvcount * w);
+  p.mode = kCinAll | kRS;
+  return launch(c, p, pl, dt, stream);
+}
+
+ddl_result_t ddl_allgather(ddl_comm_t c, const void* sendbuf, void* recvbuf, size_t sendcount, ddl_dtype_t dt,
+                           void* stream) {
+  ddl_result_t r = check_common(c, dt, DDL_SUM);
+  if (r != DDL_SUCCESS) return r;
+  if (c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  if (sendcount == 0) return DDL_SUCCESS;
+  if (!sendbuf || !recvbuf || !aligned16(sendbuf) || !aligned16(recvbuf)) return DDL_ERR_INVALID_ARGUMENT;
+  const int w = elem_size(dt);
+  if (c->P == 1) return local_copy(sendbuf, recvbuf, sendcount, dt, stream);
+  const size_t n = sendcount * (size_t)c->P;
+  if (n * w > c->max_bytes) return DDL_ERR_TOO_LARGE;
+  DDL_CUDA(cudaSetDevice(c->device));
+  const bool vec = (sendcount * w) % 16 == 0;
+  Plan pl = plan_hier(c, n, sendcount, dt, vec);
+  KParams p = base_params(c, n, DDL_SUM);
+  p.q = pl.q;
+  p.slice = pl.slice;
+  for (int m = 0; m < c->P; ++m) p.work[m] = c->stage_of(m);
+  p.cin[c->rank] = sendbuf;
+  p.cout[c->rank] = recvbuf;
+  p.mode = kCinOwn | kAG | kCoutAll;
+  return launch(c, p, pl, dt, stream);
+}
+
+ddl_result_t ddl_async_error(ddl_comm_t c) {
+  if (!c) return DDL_ERR_INVALID_ARGUMENT;
+  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_CUDA(cudaDeviceSynchronize());
+  int v = 0;
+  DDL_CUDA(cudaMemcpy(&v, c->err, sizeof(int), cudaMemcpyDeviceToHost));
+  return (ddl_result_t)v;
+}
+
+ddl_result_t ddl_set_algo(ddl_comm_t c, ddl_algo_t algo, size_t oneshot_max_bytes) {
+  if (!c || algo < DDL_ALGO_AUTO || algo > DDL_ALGO_ONESHOT) return DDL_ERR_INVALID_ARGUMENT;
+  c->algo = algo;
+  c->oneshot_max = oneshot_max_bytes;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_set_timeout(ddl_comm_t c, uint64_t timeout_ms) {
+  if (!c) return DDL_ERR_INVALID_ARGUMENT;
+  c->timeout_ns = timeout_ms * 1000000ull;
+  return DDL_SUCCESS;
+}
+
+ddl_algo_t ddl_algo_for(ddl_comm_t c, size_t count, ddl_dtype_t dt) {
+  if (!c || !valid_dtype(dt)) return DDL_ALGO_AUTO;
+  Plan pl;
+  return use_oneshot(c, count, dt, &pl) ? DDL_ALGO_ONESHOT : DDL_ALGO_HIER;
+}
+
+int ddl_ctas_for(ddl_comm_t c, size_t count, ddl_dtype_t dt) {
+  if (!c || !valid_dtype(dt) || count == 0) return 0;
+  Plan pl;
+  if (use_oneshot(c, count, dt, &pl)) return pl.nctas;
+  return plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true).nctas;
+}
+
+ddl_result_t ddl_debug_skip_rank(ddl_comm_t c, int rank) {
+  if (!c) return DDL_ERR_INVALID_ARGUMENT;
+  c->skip_rank = rank;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_finalize(ddl_comm_t c) {
+  if (!c) return DDL_SUCCESS;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int m = 0; m < kMaxRanks; ++m)
+    if (c->peer_mapped[m]) cudaIpcCloseMemHandle(c->peer_base[m]);
+  if (c->alloc) cudaFree(c->alloc);
+  if (c->lb_flags) cudaFree(c->lb_flags);
+  if (c->lb_ws) cudaFree(c->lb_ws);
+  if (c->err) cudaFree(c->err);
+  delete c;
+  return DDL_SUCCESS;
+}
+
+// ------------------------------------------------------------------ loopback
+ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, int ndims, int cuda_device) {
+  if (!comm) return DDL_ERR_INVALID_ARGUMENT;
+  *comm = nullptr;
+  ddl_comm* c = new (std::nothrow) ddl_comm();
+  if (!c) return DDL_ERR_CUDA;
+  c->loopback = true;
+  ddl_result_t r = common_init(c, nranks, dims, ndims, cuda_device);
+  if (r != DDL_SUCCESS) {
+    delete c;
+    return r;
+  }
+  cudaError_t e = cudaMalloc(&c->lb_flags, c->flags_bytes * nranks);
+  if (e == cudaSuccess) e = cudaMemset(c->lb_flags, 0, c->flags_bytes * nranks);
+  if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (c->lb_flags) cudaFree(c->lb_flags);
+    if (c->err) cudaFree(c->err);
+    delete c;
+    return cuda_fail(e, "ddl_loopback_init allocation");
+  }
+  c->connected = true;
+  *comm = c;
+  return DDL_SUCCESS;
+}
+
+static ddl_result_t check_ptrs(const ddl_comm* c, const void* const* ptrs) {
+  if (!ptrs) return DDL_ERR_INVALID_ARGUMENT;
+  for (int r = 0; r < c->P; ++r)
+    if (!ptrs[r] || !aligned16(ptrs[r])) return DDL_ERR_INVALID_ARGUMENT;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_group_allreduce(ddl_comm_t c, void* const* bufs, size_t count, ddl_dtype_t dt, ddl_op_t op,
+                                 void* stream) {
+  ddl_result_t r = check_common(c, dt, op);
+  if (r != DDL_SUCCESS) return r;
+  if (!c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  if (count == 0 || c->P == 1) return DDL_SUCCESS;
+  if ((r = check_ptrs(c, bufs)) != DDL_SUCCESS) return r;
+  DDL_CUDA(cudaSetDevice(c->device));
+  KParams p = base_params(c, count, op);
+  Plan pl;
+  const bool one = use_oneshot(c, count, dt, &pl);
+  if (!one) pl = plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true);
+  p.q = pl.q;
+  p.slice = pl.slice;
+  for (int m = 0; m < c->P; ++m) {
+    p.in[m] = bufs[m];
+    p.work[m] = bufs[m];
+    p.out[m] = bufs[m];
+  }
+  p.mode = one ? 0 : (kRS | kAG);
+  return launch(c, p, pl, dt, stream);
+}
+
+ddl_result_t ddl_group_reduce_scatter(ddl_comm_t c, const void* const* sendbufs, void* const* recvbufs,
+                                      size_t recvcount, ddl_dtype_t dt, ddl_op_t op, void* stream) {
+  ddl_result_t r = check_common(c, dt, op);
+  if (r != DDL_SUCCESS) return r;
+  if (!c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  if (recvcount == 0) return DDL_SUCCESS;
+  if ((r = check_ptrs(c, sendbufs)) != DDL_SUCCESS) return r;
+  if ((r = check_ptrs(c, recvbufs)) != DDL_SUCCESS) return r;
+  if (c->P == 1) return local_copy(sendbufs[0], recvbufs[0], recvcount, dt, stream);
+  const int w = elem_size(dt);
+  const size_t n = recvcount * (size_t)c->P;
+  DDL_CUDA(cudaSetDevice(c->device));
+  const size_t need = (n * w + 255) / 256 * 256;
+  if (need > c->lb_ws_bytes) {
+    DDL_CUDA(cudaDeviceSynchronize());
+    if (c->lb_ws) cudaFree(c->lb_ws);
+    c->lb_ws = nullptr;
+    c->lb_ws_bytes = 0;
+    DDL_CUDA(cudaMalloc(&c->lb_ws, need * c->P));
+    c->lb_ws_bytes = need;
+  }
+  const bool vec = (recvcount * w) % 16 == 0;
+  Plan pl = plan_hier(c, n, recvcount, dt, vec);
+  KParams p = base_params(c, n, op);
+  p.q = pl.q;
+  p.slice = pl.slice;
+  for (int m = 0; m < c->P; ++m) {
+    p.in[m] = sendbufs[m];
+    p.work[m] = c->lb_ws + (size_t)m * c->lb_ws_bytes;
+    p.out[m] = static_cast<char*>(recvbufs[m]) - (ptrdiff_t)m * (ptrdiff_t)(recvcount * w);
+  }
+  p.mode = kRS;
+  return launch(c, p, pl, dt, stream);
+}
+
+ddl_result_t ddl_group_allgather(ddl_comm_t c, const void* const* sendbufs, void* const* recvbufs,
+                                 size_t sendcount, ddl_dtype_t dt, void* stream) {
+  ddl_result_t r = check_common(c, dt, DDL_SUM);
+  if (r != DDL_SUCCESS) return r;
+  if (!c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  if (sendcount == 0) return DDL_SUCCESS;
+  if ((r = check_ptrs(c, sendbufs)) != DDL_SUCCESS) return r;
+  if ((r = check_ptrs(c, recvbufs)) != DDL_SUCCESS) return r;
+  if (c->P == 1) return local_copy(sendbufs[0], recvbufs[0], sendcount, dt, stream);
+  const int w = elem_size(dt);
+  const size_t n = sendcount * (size_t)c->P;
+  DDL_CUDA(cudaSetDevice(c->device));
+  const bool vec = (sendcount * w) % 16 == 0;
+  Plan pl = plan_hier(c, n, sendcount, dt, vec);
+  KParams p = base_params(c, n, DDL_SUM);
+  p.q = pl.q;
+  p.slice = pl.slice;
+  for (int m = 0; m < c->P; ++m) {
+    p.work[m] = recvbufs[m];
+    p.cin[m] = sendbufs[m];
+  }
+  p.mode = kCinOwn | kAG;
+  return launch(c, p, pl, dt, stream);
+}
+
+// ------------------------------------------------------------------ K5 local reduce
+ddl_result_t ddl_local_reduce(const void* const* ins, int g, void* out, size_t count, ddl_dtype_t dt, float scale,
+                              void* stream) {
+  if (!ins || !out || g < 1 || g > kMaxLocalIn || !valid_dtype(dt)) return DDL_ERR_INVALID_ARGUMENT;
+  if (dt == DDL_INT32 && scale != 1.0f) return DDL_ERR_UNSUPPORTED;
+  if (count == 0) return DDL_SUCCESS;
+  LRParams p;
+  std::memset(&p, 0, sizeof(p));
+  bool vec = aligned16(out);
+  for (int j = 0; j < g; ++j) {
+    if (!ins[j]) return DDL_ERR_INVALID_ARGUMENT;
+    p.in[j] = ins[j];
+    vec = vec && aligned16(ins[j]);
+  }
+  p.out = out;
+  p.n = count;
+  p.g = g;
+  p.scale = scale;
+  const void* fn;
+  if (dt == DDL_INT32) fn = vec ? (const void*)ddl_local_reduce_kernel<int32_t, true> : (const void*)ddl_local_reduce_kernel<int32_t, false>;
+  else if (dt == DDL_FLOAT32) fn = vec ? (const void*)ddl_local_reduce_kernel<float, true> : (const void*)ddl_local_reduce_kernel<float, false>;
+  else fn = vec ? (const void*)ddl_local_reduce_kernel<__nv_bfloat16, true> : (const void*)ddl_local_reduce_kernel<__nv_bfloat16, false>;
+  int dev = 0, sms = 148;
+  DDL_CUDA(cudaGetDevice(&dev));
+  DDL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int W = vec ? 16 / elem_size(dt) : 1;
+  const uint64_t items = (count + W - 1) / W;
+  uint64_t grid = (uint64_t)blocks_per_sm(fn) * sms;
+  const uint64_t need = (items + kThreads - 1) / kThreads;
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  void* args[] = {&p};
+  DDL_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kThreads), args, 0, static_cast<cudaStream_t>(stream)));
+  return DDL_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,375 @@
+"""Thin Python binding of libddl (include/ddl.h).
+
+Argument marshalling only: every step of the all-reduce runs in libddl's sm_100a kernels.
+PyTorch supplies device memory, streams and the process group used once to exchange the
+cudaIpc handles (never on the data path).  There is no CPU fallback: if libddl.so is
+missing, importing this module raises.
+
+Low-level functions carry the C names (``ddl_init``, ``ddl_allreduce``, ...) and take raw
+pointers; the classes below wrap them for torch tensors:
+
+* ``Comm``      -- one process per GPU (``init(dims)`` under torchrun).
+* ``Loopback``  -- P virtual ranks on one GPU, one launch (tests, 1-GPU benchmark).
+* ``local_reduce`` -- K5, out = scale * sum_j ins[j].
+
+``dims`` follow the paper's "2x4" notation when given as a string (outer x inner, e.g.
+"2 nodes x 4 GPUs") and are innermost-first when given as a list.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("DDL_LIB", os.path.join(HERE, "libddl.so"))
+
+SUCCESS, ERR_INVALID_ARGUMENT, ERR_BAD_DIMS, ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_PEER_ACCESS, \
+    ERR_NOT_CONNECTED, ERR_TOO_LARGE, ERR_TIMEOUT, ERR_MISMATCH = range(10)
+INT32, FLOAT32, BFLOAT16 = 0, 1, 2
+SUM, AVG = 0, 1
+ALGO_AUTO, ALGO_HIER, ALGO_ONESHOT = 0, 1, 2
+MAX_RANKS = 16
+
+DTYPE_CODES = {"int32": INT32, "float32": FLOAT32, "bfloat16": BFLOAT16}
+OP_CODES = {"sum": SUM, "avg": AVG}
+
+
+class DDLError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        msg = _lib.ddl_result_string(code).decode()
+        extra = _lib.ddl_last_error_string().decode() if code == ERR_CUDA else ""
+        super().__init__(f"{what}: {msg}" + (f" ({extra})" if extra else ""))
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libddl.so not built at {LIB_PATH}: run ./build.sh (or __graft_entry__.build())")
+    lib = ctypes.CDLL(LIB_PATH)
+    c_int, c_size, c_void, c_u64 = ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint64
+    ip = ctypes.POINTER(c_int)
+    pp = ctypes.POINTER(c_void)
+    sig = {
+        "ddl_version": (c_int, []),
+        "ddl_result_string": (ctypes.c_char_p, [c_int]),
+        "ddl_last_error_string": (ctypes.c_char_p, []),
+        "ddl_check_dims": (c_int, [c_int, ip, c_int]),
+        "ddl_block_elems": (c_size, [c_size, c_int, c_int]),
+        "ddl_plan_group": (c_int, [c_int, ip, c_int, c_int, c_int, ip]),
+        "ddl_plan_blocks": (c_int, [c_int, ip, c_int, c_int, c_int, ip, ip]),
+        "ddl_plan_barriers": (c_int, [c_int, ip, c_int, c_int, ip, ip, ip]),
+        "ddl_plan_traffic": (c_int, [c_size, c_int, c_int, ip, c_int, c_int,
+                                     ctypes.POINTER(c_u64), ctypes.POINTER(c_u64)]),
+        "ddl_init": (c_int, [pp, c_int, c_int, ip, c_int, c_int, c_size]),
+        "ddl_handle_size": (c_size, []),
+        "ddl_export_handle": (c_int, [c_void, c_void]),
+        "ddl_connect": (c_int, [c_void, c_void]),
+        "ddl_buffer": (c_int, [c_void, pp, ctypes.POINTER(c_size)]),
+        "ddl_allreduce": (c_int, [c_void, c_void, c_size, c_int, c_int, c_void]),
+        "ddl_reduce_scatter": (c_int, [c_void, c_void, c_void, c_size, c_int, c_int, c_void]),
+        "ddl_allgather": (c_int, [c_void, c_void, c_void, c_size, c_int, c_void]),
+        "ddl_async_error": (c_int, [c_void]),
+        "ddl_set_algo": (c_int, [c_void, c_int, c_size]),
+        "ddl_set_timeout": (c_int, [c_void, c_u64]),
+        "ddl_algo_for": (c_int, [c_void, c_size, c_int]),
+        "ddl_ctas_for": (c_int, [c_void, c_size, c_int]),
+        "ddl_debug_skip_rank": (c_int, [c_void, c_int]),
+        "ddl_finalize": (c_int, [c_void]),
+        "ddl_loopback_init": (c_int, [pp, c_int, ip, c_int, c_int]),
+        "ddl_group_allreduce": (c_int, [c_void, pp, c_size, c_int, c_int, c_void]),
+        "ddl_group_reduce_scatter": (c_int, [c_void, pp, pp, c_size, c_int, c_int, c_void]),
+        "ddl_group_allgather": (c_int, [c_void, pp, pp, c_size, c_int, c_void]),
+        "ddl_local_reduce": (c_int, [pp, c_int, c_void, c_size, c_int, ctypes.c_float, c_void]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def _check(code: int, what: str) -> None:
+    if code != SUCCESS:
+        raise DDLError(code, what)
+
+
+def _ints(xs) -> ctypes.Array:
+    return (ctypes.c_int * max(1, len(xs)))(*xs)
+
+
+def _ptrs(xs) -> ctypes.Array:
+    return (ctypes.c_void_p * max(1, len(xs)))(*xs)
+
+
+def parse_dims(spec, nranks: int | None = None) -> list[int]:
+    """'2x4' -> [4, 2] (written outer x inner); a list is already innermost-first;
+    None -> [nranks] (one flat dimension)."""
+    if spec is None:
+        return [int(nranks)]
+    if isinstance(spec, str):
+        return [int(x) for x in spec.lower().split("x")][::-1]
+    return [int(g) for g in spec]
+
+
+# ---------------------------------------------------------------- host planner queries
+def check_dims(nranks: int, dims) -> int:
+    return _lib.ddl_check_dims(nranks, _ints(dims), len(dims))
+
+
+def block_elems(count: int, nranks: int, dtype: str) -> int:
+    return _lib.ddl_block_elems(count, nranks, DTYPE_CODES[dtype])
+
+
+def plan_group(nranks: int, dims, rank: int, d: int) -> list[int]:
+    out = (ctypes.c_int * dims[d])()
+    _check(_lib.ddl_plan_group(nranks, _ints(dims), len(dims), rank, d, out), "ddl_plan_group")
+    return list(out)
+
+
+def plan_blocks(nranks: int, dims, rank: int, d: int) -> list[int]:
+    out = (ctypes.c_int * nranks)()
+    nb = ctypes.c_int()
+    _check(_lib.ddl_plan_blocks(nranks, _ints(dims), len(dims), rank, d, out, ctypes.byref(nb)),
+           "ddl_plan_blocks")
+    return list(out[:nb.value])
+
+
+def plan_barriers(nranks: int, dims, rank: int) -> list[list[int]]:
+    nmax = 2 * len(dims) + 1
+    peers = (ctypes.c_int * (nmax * nranks))()
+    counts = (ctypes.c_int * nmax)()
+    nb = ctypes.c_int()
+    _check(_lib.ddl_plan_barriers(nranks, _ints(dims), len(dims), rank, peers, counts, ctypes.byref(nb)),
+           "ddl_plan_barriers")
+    return [list(peers[j * nranks:j * nranks + counts[j]]) for j in range(nb.value)]
+
+
+def plan_traffic(count: int, dtype: str, nranks: int, dims, rank: int) -> tuple[list[int], list[int]]:
+    k = len(dims)
+    rs = (ctypes.c_uint64 * k)()
+    ag = (ctypes.c_uint64 * k)()
+    _check(_lib.ddl_plan_traffic(count, DTYPE_CODES[dtype], nranks, _ints(dims), k, rank, rs, ag),
+           "ddl_plan_traffic")
+    return list(rs), list(ag)
+
+
+# ---------------------------------------------------------------- torch helpers
+def _torch():
+    import torch
+    return torch
+
+
+def dtype_name(t) -> str:
+    torch = _torch()
+    m = {torch.int32: "int32", torch.float32: "float32", torch.bfloat16: "bfloat16"}
+    if t.dtype not in m:
+        raise DDLError(ERR_UNSUPPORTED, f"dtype {t.dtype}")
+    return m[t.dtype]
+
+
+def _stream(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _require_cuda(t) -> None:
+    if not t.is_cuda or not t.is_contiguous():
+        raise DDLError(ERR_INVALID_ARGUMENT, "tensors must be contiguous CUDA tensors")
+
+
+# ---------------------------------------------------------------- multi-process comm
+def exchange_handles(dims, mine: bytes, group=None) -> bytes:
+    """Bootstrap exchange (never on the data path): all-gather every rank's (dims, handle
+    bytes) over the process group, check all ranks agree on dims, return the handles
+    concatenated in rank order."""
+    import torch.distributed as dist
+    n = dist.get_world_size(group)
+    allh = [None] * n
+    dist.all_gather_object(allh, (list(dims), bytes(mine)), group=group)
+    if any(d != list(dims) for d, _ in allh):
+        raise DDLError(ERR_MISMATCH, "ranks passed different dims")
+    if any(len(b) != len(mine) for _, b in allh):
+        raise DDLError(ERR_MISMATCH, "handle sizes differ between ranks")
+    return b"".join(b for _, b in allh)
+
+
+class Comm:
+    """One rank of a DDL communicator (one process per GPU).  Collective construction:
+    every rank of ``group`` calls ``Comm(dims, ...)``; cudaIpc handles are exchanged with
+    ``all_gather_object`` on the (gloo or NCCL) process group -- bootstrap only."""
+
+    def __init__(self, dims=None, group=None, max_bytes: int = 256 << 20, device: int | None = None):
+        torch = _torch()
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.nranks = dist.get_world_size(group)
+        self.dims = parse_dims(dims, self.nranks)
+        if math.prod(self.dims) != self.nranks:
+            raise DDLError(ERR_BAD_DIMS, f"dims {self.dims} vs {self.nranks} ranks")
+        self.device = torch.cuda.current_device() if device is None else device
+        h = ctypes.c_void_p()
+        _check(_lib.ddl_init(ctypes.byref(h), self.rank, self.nranks, _ints(self.dims), len(self.dims),
+                             self.device, max_bytes), "ddl_init")
+        self.h = h
+        hs = _lib.ddl_handle_size()
+        mine = ctypes.create_string_buffer(hs)
+        _check(_lib.ddl_export_handle(self.h, mine), "ddl_export_handle")
+        blob = ctypes.create_string_buffer(exchange_handles(self.dims, bytes(mine.raw), group), hs * self.nranks)
+        _check(_lib.ddl_connect(self.h, blob), "ddl_connect")
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _check(_lib.ddl_buffer(self.h, ctypes.byref(p), ctypes.byref(n)), "ddl_buffer")
+        self.buffer_ptr, self.buffer_bytes = p.value, n.value
+
+    def buffer(self, count: int, dtype, offset_bytes: int = 0):
+        """A torch tensor view of the symmetric zero-copy buffer (same offset on every rank)."""
+        torch = _torch()
+        esz = torch.tensor([], dtype=dtype).element_size()
+        if offset_bytes % 256 or offset_bytes + count * esz > self.buffer_bytes:
+            raise DDLError(ERR_TOO_LARGE, "view outside the symmetric buffer")
+        full = _tensor_from_ptr(self.buffer_ptr, self.buffer_bytes, self.device)
+        return full[offset_bytes:offset_bytes + count * esz].view(dtype)
+
+    def all_reduce(self, t, op: str = "sum", stream=None):
+        _require_cuda(t)
+        _check(_lib.ddl_allreduce(self.h, t.data_ptr(), t.numel(), DTYPE_CODES[dtype_name(t)], OP_CODES[op],
+                                  _stream(stream)), "ddl_allreduce")
+        return t
+
+    def reduce_scatter(self, out, inp, op: str = "sum", stream=None):
+        _require_cuda(out)
+        _require_cuda(inp)
+        if inp.numel() != out.numel() * self.nranks or inp.dtype != out.dtype:
+            raise DDLError(ERR_INVALID_ARGUMENT, "reduce_scatter: inp must hold nranks * out.numel()")
+        _check(_lib.ddl_reduce_scatter(self.h, inp.data_ptr(), out.data_ptr(), out.numel(),
+                                       DTYPE_CODES[dtype_name(out)], OP_CODES[op], _stream(stream)),
+               "ddl_reduce_scatter")
+        return out
+
+    def all_gather(self, out, inp, stream=None):
+        _require_cuda(out)
+        _require_cuda(inp)
+        if out.numel() != inp.numel() * self.nranks or inp.dtype != out.dtype:
+            raise DDLError(ERR_INVALID_ARGUMENT, "all_gather: out must hold nranks * inp.numel()")
+        _check(_lib.ddl_allgather(self.h, inp.data_ptr(), out.data_ptr(), inp.numel(),
+                                  DTYPE_CODES[dtype_name(out)], _stream(stream)), "ddl_allgather")
+        return out
+
+    def set_algo(self, algo: int, oneshot_max_bytes: int = 256 << 10) -> None:
+        _check(_lib.ddl_set_algo(self.h, algo, oneshot_max_bytes), "ddl_set_algo")
+
+    def async_error(self) -> int:
+        return _lib.ddl_async_error(self.h)
+
+    def finalize(self) -> None:
+        if self.h:
+            import torch.distributed as dist
+            _torch().cuda.synchronize()
+            dist.barrier(group=self.group)
+            _lib.ddl_finalize(self.h)
+            self.h = None
+
+
+def init(dims=None, group=None, max_bytes: int = 256 << 20) -> Comm:
+    """``ddl.init(dims)``: the analogue of the paper's ``import ddl`` + ``ddlrun`` setup
+     under torchrun."""
+    return Comm(dims, group, max_bytes)
+
+
+def _tensor_from_ptr(ptr: int, nbytes: int, device: int):
+    """Wrap library-owned device memory as a uint8 torch tensor (no copy, not owned)."""
+    torch = _torch()
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CAI(), device=f"cuda:{device}")
+
+
+# ---------------------------------------------------------------- loopback (1 GPU)
+class Loopback:
+    """P virtual ranks on one GPU: the same kernels and barrier protocol as ``Comm``,
+    launched once for all ranks (cooperative launch)."""
+
+    def __init__(self, nranks: int, dims=None, device: int | None = None):
+        torch = _torch()
+        self.nranks = nranks
+        self.dims = parse_dims(dims, nranks)
+        self.device = torch.cuda.current_device() if device is None else device
+        h = ctypes.c_void_p()
+        _check(_lib.ddl_loopback_init(ctypes.byref(h), nranks, _ints(self.dims), len(self.dims), self.device),
+               "ddl_loopback_init")
+        self.h = h
+
+    def all_reduce(self, bufs, op: str = "sum", stream=None):
+        for b in bufs:
+            _require_cuda(b)
+        _check(_lib.ddl_group_allreduce(self.h, _ptrs([b.data_ptr() for b in bufs]), bufs[0].numel(),
+                                        DTYPE_CODES[dtype_name(bufs[0])], OP_CODES[op], _stream(stream)),
+               "ddl_group_allreduce")
+        return bufs
+
+    def reduce_scatter(self, outs, inps, op: str = "sum", stream=None):
+        _check(_lib.ddl_group_reduce_scatter(self.h, _ptrs([t.data_ptr() for t in inps]),
+                                             _ptrs([t.data_ptr() for t in outs]), outs[0].numel(),
+                                             DTYPE_CODES[dtype_name(outs[0])], OP_CODES[op], _stream(stream)),
+               "ddl_group_reduce_scatter")
+        return outs
+
+    def all_gather(self, outs, inps, stream=None):
+        _check(_lib.ddl_group_allgather(self.h, _ptrs([t.data_ptr() for t in inps]),
+                                        _ptrs([t.data_ptr() for t in outs]), inps[0].numel(),
+                                        DTYPE_CODES[dtype_name(outs[0])], _stream(stream)),
+               "ddl_group_allgather")
+        return outs
+
+    def set_algo(self, algo: int, oneshot_max_bytes: int = 256 << 10) -> None:
+        _check(_lib.ddl_set_algo(self.h, algo, oneshot_max_bytes), "ddl_set_algo")
+
+    def set_timeout(self, ms: int) -> None:
+        _check(_lib.ddl_set_timeout(self.h, ms), "ddl_set_timeout")
+
+    def algo_for(self, count: int, dtype: str) -> int:
+        return _lib.ddl_algo_for(self.h, count, DTYPE_CODES[dtype])
+
+    def ctas_for(self, count: int, dtype: str) -> int:
+        return _lib.ddl_ctas_for(self.h, count, DTYPE_CODES[dtype])
+
+    def debug_skip_rank(self, r: int) -> None:
+        _check(_lib.ddl_debug_skip_rank(self.h, r), "ddl_debug_skip_rank")
+
+    def async_error(self) -> int:
+        return _lib.ddl_async_error(self.h)
+
+    def finalize(self) -> None:
+        if self.h:
+            _lib.ddl_finalize(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.finalize()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- K5
+def local_reduce(ins, out, scale: float = 1.0, stream=None):
+    """out = scale * sum_j ins[j] (ascending j), the 1-GPU HBM-roofline kernel."""
+    for t in list(ins) + [out]:
+        _require_cuda(t)
+    _check(_lib.ddl_local_reduce(_ptrs([t.data_ptr() for t in ins]), len(ins), out.data_ptr(), out.numel(),
+                                 DTYPE_CODES[dtype_name(out)], float(scale), _stream(stream)),
+           "ddl_local_reduce")
+    return out
