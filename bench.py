@@ -213,15 +213,17 @@ def run_loopback(args):
             if evs is not None:
                 evs[b][1].record(stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    assert lb.async_error() == ddl.SUCCESS
-
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nb)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
+    with ClockSampler(0) as clk:   # sampling spans warm-up + timed region (>= a few 100-ms samples)
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize()
+        assert lb.async_error() == ddl.SUCCESS
+        t_pad = time.perf_counter()
+        while time.perf_counter() - t_pad < 0.3:   # keep the GPU busy so the sampler sees load clocks
+            step()
+            torch.cuda.synchronize()
         t_start.record(stream)
         for k in range(args.steps):
             step(evs[k])
@@ -401,7 +403,7 @@ def run_multi(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ddl", choices=["ddl", "reference"])
     ap.add_argument("--dims", default=None, help="override the factorisation, e.g. 2x2x2")

@@ -146,12 +146,16 @@ __device__ __forceinline__ uint4 ld_vec(const char* p) { return __ldcg(reinterpr
 __device__ __forceinline__ void st_vec(char* p, const uint4& v) { *reinterpret_cast<uint4*>(p) = v; }
 
 // ------------------------------------------------------------------------ device barrier (K4)
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// Flag signal / poll.  Across GPUs the scope must be .sys; in loopback mode every agent is
+// on this GPU and .gpu scope suffices (a cheaper MEMBAR).
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v, bool gpu_scope) {
+  if (gpu_scope) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p, bool gpu_scope) {
   uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  if (gpu_scope) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -172,11 +176,11 @@ __device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int
   int fail = 0;
   if (threadIdx.x < np) {
     const int m = peer(threadIdx.x);
-    st_release_sys(flag_slot(p, p.flags[m], slot, blockIdx.x, me), epoch);
+    st_release(flag_slot(p, p.flags[m], slot, blockIdx.x, me), epoch, p.loopback);
     const uint32_t* f = flag_slot(p, p.flags[me], slot, blockIdx.x, m);
     uint64_t t0 = 0;
     uint32_t spins = 0;
-    while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
+    while ((int32_t)(ld_acquire(f, p.loopback) - epoch) < 0) {
       if ((++spins & 1023u) == 0) {
         const uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
@@ -384,9 +388,266 @@ __device__ __forceinline__ void ag_phase(const KParams& p, int me, int d) {
   }
 }
 
+// ------------------------------------------------------------------------ TMA-staged phases
+// The 16-byte-vector path of every phase (RS, AG, copy-in/out) runs through a kStages-deep
+// shared-memory ring filled by bulk asynchronous copies (cp.async.bulk, the TMA engine's
+// linear mode) from local or peer-mapped global memory.  One elected thread issues the
+// copies and arms an mbarrier per stage with the expected byte count; all 512 threads wait
+// on it, fold the g staged segments in ascending member order from shared memory, and
+// store the result with 16-byte st.global.  Bytes in flight per SM = CTAs/SM * kStages *
+// kStageBytes (default 2 * 2 * 48 KB), independent of registers -- the latency-hiding budget
+// HBM and NVLink need (round-1 ncu: the register-staged path sat at 16 warps/SM and 48% of
+// DRAM peak).  Defaults picked by the stage/size sweep in profiles/r01_tma_sweep.txt.
+#ifndef DDL_TMA_STAGES
+#define DDL_TMA_STAGES 2
+#endif
+#ifndef DDL_TMA_STAGE_KB
+#define DDL_TMA_STAGE_KB 48
+#endif
+#ifndef DDL_TMA_MINBLOCKS
+#define DDL_TMA_MINBLOCKS 2
+#endif
+constexpr int kStages = DDL_TMA_STAGES;
+constexpr uint32_t kStageBytes = DDL_TMA_STAGE_KB * 1024;
+constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DDL_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra DDL_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// Make data that generic-proxy stores (this CTA's or a peer's, acquired through a device
+// barrier) visible to this thread's subsequent async-proxy (bulk copy) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+struct Pipe {
+  char* smem;
+  uint64_t* bar;
+  uint32_t seq;  // chunks consumed so far by this CTA (identical in every thread)
+};
+
+__device__ __forceinline__ void pipe_init(Pipe& pp) {
+  extern __shared__ __align__(128) char dsmem[];
+  pp.smem = dsmem;
+  pp.bar = reinterpret_cast<uint64_t*>(dsmem + (size_t)kStages * kStageBytes);
+  pp.seq = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&pp.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+enum PhaseKind : int { kPhRS = 0, kPhAG = 1, kPhCin = 2, kPhCinOwn = 3, kPhCout = 4 };
+
+struct PhaseCtx {
+  int kind, d, g, nunits, nb, c;
+  bool first, last;
+};
+
+__device__ __forceinline__ PhaseCtx phase_ctx(const KParams& p, int me, int kind, int d, bool first, bool last) {
+  const Topo& t = p.t;
+  PhaseCtx x;
+  x.kind = kind;
+  x.d = d;
+  x.first = first;
+  x.last = last;
+  x.c = 0;
+  x.nb = 0;
+  x.g = 1;
+  if (kind == kPhRS) {
+    x.g = t.g[d];
+    x.nb = nblocks(t, d + 1);
+    x.nunits = x.nb;
+  } else if (kind == kPhAG) {
+    x.c = coord(t, me, d);
+    x.nb = nblocks(t, d + 1);
+    x.nunits = (t.g[d] - 1) * x.nb;
+  } else if (kind == kPhCinOwn) {
+    x.nunits = 1;
+  } else {
+    x.nunits = t.P;
+  }
+  return x;
+}
+
+// Block of unit u; for AG also the source rank.
+__device__ __forceinline__ int unit_block(const KParams& p, int me, const PhaseCtx& x, int u, int* srank) {
+  const Topo& t = p.t;
+  *srank = me;
+  switch (x.kind) {
+    case kPhRS: return block_of(t, me, x.d + 1, u);
+    case kPhAG: {
+      const int l = u / x.nb;
+      const int bi = u - l * x.nb;
+      const int m = member(t, me, x.d, l < x.c ? l : l + 1);
+      *srank = m;
+      return block_of(t, m, x.d + 1, bi);
+    }
+    case kPhCinOwn: return me;
+    default: return u;
+  }
+}
+
+// Base of source v of a unit (element offsets apply on top).
+template <typename T>
+__device__ __forceinline__ const char* src_base(const KParams& p, int me, const PhaseCtx& x, int v, int srank) {
+  switch (x.kind) {
+    case kPhRS: {
+      const int m = member(p.t, me, x.d, v);
+      return static_cast<const char*>(x.first ? p.in[m] : p.work[m]);
+    }
+    case kPhAG: return static_cast<const char*>(p.work[srank]);
+    case kPhCin: return static_cast<const char*>(p.cin[me]);
+    case kPhCinOwn: return static_cast<const char*>(p.cin[me]) - (size_t)me * p.q * sizeof(T);
+    default: return static_cast<const char*>(p.work[me]);
+  }
+}
+__device__ __forceinline__ char* dst_base(const KParams& p, int me, const PhaseCtx& x) {
+  switch (x.kind) {
+    case kPhRS: return static_cast<char*>(x.last ? p.out[me] : p.work[me]);
+    case kPhCout: return static_cast<char*>(p.cout[me]);
+    default: return static_cast<char*>(p.work[me]);
+  }
+}
+
+struct UnitDesc {
+  uint64_t e0;     // first element of this CTA's slice of the unit's block
+  uint32_t bytes;  // whole 16-byte vectors, in bytes
+  uint32_t rem;    // ragged elements after them
+  int srank;       // AG: source rank
+  int pad;
+};
+
+template <typename T>
+__device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = Tr<T>::W;
+  __shared__ UnitDesc s_units[kMaxRanks];
+  const uint32_t CB = (kStageBytes / (uint32_t)x.g) & ~15u;  // bytes per source per stage
+  const bool do_scale = x.kind == kPhRS && x.last && p.op == kAvg;
+  char* dst = dst_base(p, me, x);
+
+  __syncthreads();  // the previous phase's readers of s_units are done
+  if ((int)threadIdx.x < x.nunits) {
+    int sr;
+    const Span sp = slice_span<W>(p, unit_block(p, me, x, threadIdx.x, &sr));
+    s_units[threadIdx.x] = UnitDesc{sp.e0, sp.nvec * 16u, sp.rem, sr, 0};
+  }
+  __syncthreads();
+  uint32_t total = 0;
+  for (int u = 0; u < x.nunits; ++u) total += (s_units[u].bytes + CB - 1) / CB;
+
+  // producer state (thread 0 only): next unit / byte offset to issue
+  int pu = 0;
+  uint32_t poff = 0;
+  auto issue = [&](uint32_t sq) {
+    while (poff >= s_units[pu].bytes) {
+      ++pu;
+      poff = 0;
+    }
+    const UnitDesc ud = s_units[pu];
+    const uint32_t bytes = min(CB, ud.bytes - poff);
+    const int st = (int)(sq % kStages);
+    char* sbase = pp.smem + (size_t)st * kStageBytes;
+    mbar_arm(&pp.bar[st], bytes * (uint32_t)x.g);
+    for (int v = 0; v < x.g; ++v)
+      tma_load(sbase + (size_t)v * CB, src_base<T>(p, me, x, v, ud.srank) + ud.e0 * sizeof(T) + poff, bytes,
+               &pp.bar[st]);
+    poff += bytes;
+  };
+  if (threadIdx.x == 0 && total) {
+    fence_proxy_async_global();
+    for (uint32_t j = 0; j < total && j < (uint32_t)kStages; ++j) issue(pp.seq + j);
+  }
+
+  int cu = 0;
+  uint32_t coff = 0;
+  for (uint32_t j = 0; j < total; ++j) {
+    while (coff >= s_units[cu].bytes) {
+      ++cu;
+      coff = 0;
+    }
+    const uint32_t bytes = min(CB, s_units[cu].bytes - coff);
+    const uint32_t sq = pp.seq + j;
+    const int st = (int)(sq % kStages);
+    const char* sbase = pp.smem + (size_t)st * kStageBytes;
+    char* pd = dst + s_units[cu].e0 * sizeof(T) + coff;
+    mbar_wait(&pp.bar[st], (sq / kStages) & 1u);
+    const uint32_t nv = bytes / 16u;
+    if (x.kind == kPhRS) {
+      for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+        A acc[W];
+        unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)i * 16), acc);
+        for (int v = 1; v < x.g; ++v) {
+          A y[W];
+          unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)v * CB + (size_t)i * 16), y);
+#pragma unroll
+          for (int k = 0; k < W; ++k) acc[k] = Tr<T>::add(acc[k], y[k]);
+        }
+        if (do_scale) {
+#pragma unroll
+          for (int k = 0; k < W; ++k) acc[k] = Tr<T>::mul(acc[k], p.scale);
+        }
+        st_vec(pd + (size_t)i * 16, pack<T>(acc));
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x)
+        st_vec(pd + (size_t)i * 16, *reinterpret_cast<const uint4*>(sbase + (size_t)i * 16));
+    }
+    coff += bytes;
+    __syncthreads();  // every thread is done with stage st
+    if (threadIdx.x == 0 && j + kStages < total) issue(sq + kStages);
+  }
+  pp.seq += total;
+
+  // ragged remainders (< 16 B where a slice is cut by n), element by element
+  for (int u = 0; u < x.nunits; ++u) {
+    const UnitDesc ud = s_units[u];
+    if (threadIdx.x < ud.rem) {
+      const size_t o = (ud.e0 + (size_t)ud.bytes / sizeof(T) + threadIdx.x) * sizeof(T);
+      if (x.kind == kPhRS) {
+        A a = 0;
+        for (int v = 0; v < x.g; ++v) {
+          const A y = Tr<T>::to(ld_elem<T>(src_base<T>(p, me, x, v, ud.srank) + o));
+          a = v == 0 ? y : Tr<T>::add(a, y);
+        }
+        if (do_scale) a = Tr<T>::mul(a, p.scale);
+        st_elem<T>(dst + o, Tr<T>::from(a));
+      } else {
+        st_elem<T>(dst + o, ld_elem<T>(src_base<T>(p, me, x, 0, ud.srank) + o));
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------ the hierarchical kernel
-template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads, 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
+// PATH: 0 = element-wise loads (unaligned RS/AG layouts), 1 = 16-byte register-staged
+// loads, 2 = 16-byte TMA-staged (default).
+template <typename T, int PATH>
+__global__ void __launch_bounds__(kThreads, PATH == 2 ? DDL_TMA_MINBLOCKS : 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
+  constexpr bool VEC = PATH >= 1;
   const int me = p.loopback ? (int)blockIdx.y : p.rank;
   const uint32_t e = next_epoch(p, me);
   if (me == p.skip_rank) return;
@@ -394,29 +655,43 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_hier_kernel(const __grid_cons
   const int L = t.nlive;
   const int me_ = me;
   auto group_peer = [&](int j) { return [&p, me_, j](int l) { return barrier_peer(p.t, me_, j, l); }; };
+  Pipe pp;
+  if constexpr (PATH == 2) pipe_init(pp);
 
-  if (p.mode & kCinAll)
-    for (int b = 0; b < t.P; ++b)
-      copy_block<T, VEC>(p, static_cast<const char*>(p.cin[me]), static_cast<char*>(p.work[me]), b, 0);
-  if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T))
-    copy_block<T, VEC>(p, static_cast<const char*>(p.cin[me]), static_cast<char*>(p.work[me]), me,
-                       (int64_t)me * (int64_t)p.q);
+  if (p.mode & kCinAll) {
+    if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhCin, 0, false, false), pp);
+    else
+      for (int b = 0; b < t.P; ++b)
+        copy_block<T, VEC>(p, static_cast<const char*>(p.cin[me]), static_cast<char*>(p.work[me]), b, 0);
+  }
+  if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T)) {
+    if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhCinOwn, 0, false, false), pp);
+    else
+      copy_block<T, VEC>(p, static_cast<const char*>(p.cin[me]), static_cast<char*>(p.work[me]), me,
+                         (int64_t)me * (int64_t)p.q);
+  }
   if (p.mode & kRS) {
     for (int j = 0; j < L; ++j) {
       if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
-      rs_dispatch<T, VEC>(p, me, t.live[j], j == 0, j == L - 1);
+      if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1), pp);
+      else rs_dispatch<T, VEC>(p, me, t.live[j], j == 0, j == L - 1);
     }
   }
   if (p.mode & kAG) {
     for (int jj = 0; jj < L; ++jj) {
       const int j = L + jj;
       if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
-      ag_phase<T, VEC>(p, me, t.live[L - 1 - jj]);
+      if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false), pp);
+      else ag_phase<T, VEC>(p, me, t.live[L - 1 - jj]);
     }
   }
-  if (p.mode & kCoutAll)
-    for (int b = 0; b < t.P; ++b)
-      copy_block<T, VEC>(p, static_cast<const char*>(p.work[me]), static_cast<char*>(p.cout[me]), b, 0);
+  if (p.mode & kCoutAll) {
+    __syncthreads();
+    if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhCout, 0, false, false), pp);
+    else
+      for (int b = 0; b < t.P; ++b)
+        copy_block<T, VEC>(p, static_cast<const char*>(p.work[me]), static_cast<char*>(p.cout[me]), b, 0);
+  }
   if (L > 0) dbarrier(p, me, 2 * L, barrier_npeers(t, 2 * L), e, group_peer(2 * L));
 }
 

@@ -91,6 +91,8 @@ struct ddl_comm {
   int ctas_limit = 0;  // 0 = occupancy bound
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int skip_rank = -1;
+  bool use_tma = true;
+  size_t tma_min_slice_bytes = 32 << 10;  // TMA path only when per-CTA slices are at least this big
 
   uint32_t* flags_of(int r) const {
     if (loopback) return reinterpret_cast<uint32_t*>(lb_flags + (size_t)r * flags_bytes);
@@ -103,14 +105,15 @@ struct ddl_comm {
 namespace {
 
 // Resident CTAs (kThreads each) per SM for a kernel, cached.
-int blocks_per_sm(const void* fn) {
+int blocks_per_sm(const void* fn, size_t smem = 0) {
   static std::mutex mu;
   static std::unordered_map<const void*, int> cache;
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(fn);
   if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) nb = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess) nb = 1;
   if (nb < 1) nb = 1;
   cache[fn] = nb;
   return nb;
@@ -121,6 +124,8 @@ void apply_env(ddl_comm* c) {
   c->oneshot_max = env_size("DDL_ONESHOT_MAX_BYTES", c->oneshot_max);
   c->min_slice_bytes = env_size("DDL_MIN_SLICE_BYTES", c->min_slice_bytes);
   c->ctas_limit = (int)env_size("DDL_CTAS", 0);
+  c->use_tma = env_size("DDL_NO_TMA", 0) == 0;
+  c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
     else if (!std::strcmp(a, "oneshot")) c->algo = DDL_ALGO_ONESHOT;
@@ -151,12 +156,14 @@ struct Plan {
   uint64_t slice = 0;
   int nctas = 0;
   bool vec = true;
+  int path = 2;  // hierarchical kernel variant: 0 element-wise, 1 register-staged, 2 TMA-staged
   bool oneshot = false;
 };
 
 template <typename T>
-const void* hier_fn(bool vec) {
-  return vec ? (const void*)ddl_hier_kernel<T, true> : (const void*)ddl_hier_kernel<T, false>;
+const void* hier_fn(int path) {
+  if (path == 2) return (const void*)ddl_hier_kernel<T, 2>;
+  return path == 1 ? (const void*)ddl_hier_kernel<T, 1> : (const void*)ddl_hier_kernel<T, 0>;
 }
 template <typename T>
 const void* oneshot_fn(int K) {
@@ -168,11 +175,12 @@ const void* oneshot_fn(int K) {
     default: return nullptr;
   }
 }
-const void* hier_fn_dt(ddl_dtype_t dt, bool vec) {
-  if (dt == DDL_INT32) return hier_fn<int32_t>(vec);
-  if (dt == DDL_FLOAT32) return hier_fn<float>(vec);
-  return hier_fn<__nv_bfloat16>(vec);
+const void* hier_fn_dt(ddl_dtype_t dt, int path) {
+  if (dt == DDL_INT32) return hier_fn<int32_t>(path);
+  if (dt == DDL_FLOAT32) return hier_fn<float>(path);
+  return hier_fn<__nv_bfloat16>(path);
 }
+size_t hier_smem(int path) { return path == 2 ? kTmaSmem : 0; }
 const void* oneshot_fn_dt(ddl_dtype_t dt, int K) {
   if (dt == DDL_INT32) return oneshot_fn<int32_t>(K);
   if (dt == DDL_FLOAT32) return oneshot_fn<float>(K);
@@ -180,8 +188,8 @@ const void* oneshot_fn_dt(ddl_dtype_t dt, int K) {
 }
 
 // CTAs per rank that may be resident at once (loopback: all P ranks share the GPU).
-int cap_per_rank(const ddl_comm* c, const void* fn) {
-  int cap = blocks_per_sm(fn) * c->num_sms;
+int cap_per_rank(const ddl_comm* c, const void* fn, size_t smem = 0) {
+  int cap = blocks_per_sm(fn, smem) * c->num_sms;
   if (c->loopback) cap /= c->P;
   if (c->ctas_limit > 0 && c->ctas_limit < cap) cap = c->ctas_limit;
   if (cap > c->cmax) cap = c->cmax;
@@ -194,7 +202,13 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
   pl.vec = vec;
   const int w = elem_size(dt);
   const uint64_t W = vec ? 16 / w : 1;
-  const int cap = cap_per_rank(c, hier_fn_dt(dt, vec));
+  pl.path = !vec ? 0 : (c->use_tma ? 2 : 1);
+  int cap = cap_per_rank(c, hier_fn_dt(dt, pl.path), hier_smem(pl.path));
+  if (pl.path == 2 && q * w < c->tma_min_slice_bytes * (uint64_t)cap) {
+    // small per-CTA slices: the register-staged path has lower per-phase latency
+    pl.path = 1;
+    cap = cap_per_rank(c, hier_fn_dt(dt, 1), 0);
+  }
   uint64_t want = (q * w + c->min_slice_bytes - 1) / c->min_slice_bytes;
   if (want < 1) want = 1;
   if (want > (uint64_t)cap) want = cap;
@@ -247,18 +261,20 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
 }
 
 ddl_result_t launch(const ddl_comm* c, const KParams& p, const Plan& pl, ddl_dtype_t dt, void* stream) {
-  const void* fn = pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive) : hier_fn_dt(dt, pl.vec);
+  const void* fn = pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive) : hier_fn_dt(dt, pl.path);
   if (!fn) return DDL_ERR_UNSUPPORTED;
+  const size_t smem = pl.oneshot ? 0 : hier_smem(pl.path);
+  blocks_per_sm(fn, smem);  // sets the dynamic shared-memory attribute once
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void* args[] = {const_cast<KParams*>(&p)};
   if (std::getenv("DDL_DEBUG"))
-    std::fprintf(stderr, "[ddl] %s n=%llu q=%llu slice=%llu ctas=%d vec=%d mode=%d P=%d loopback=%d\n",
+    std::fprintf(stderr, "[ddl] %s n=%llu q=%llu slice=%llu ctas=%d path=%d mode=%d P=%d loopback=%d\n",
                  pl.oneshot ? "oneshot" : "hier", (unsigned long long)p.n, (unsigned long long)p.q,
-                 (unsigned long long)p.slice, pl.nctas, (int)pl.vec, p.mode, c->P, (int)c->loopback);
+                 (unsigned long long)p.slice, pl.nctas, pl.path, p.mode, c->P, (int)c->loopback);
   if (c->loopback) {
-    DDL_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pl.nctas, c->P), dim3(kThreads), args, 0, s));
+    DDL_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pl.nctas, c->P), dim3(kThreads), args, smem, s));
   } else {
-    DDL_CUDA(cudaLaunchKernel(fn, dim3(pl.nctas), dim3(kThreads), args, 0, s));
+    DDL_CUDA(cudaLaunchKernel(fn, dim3(pl.nctas), dim3(kThreads), args, smem, s));
   }
   return DDL_SUCCESS;
 }
