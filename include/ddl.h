@@ -155,6 +155,13 @@ int ddl_ctas_for(ddl_comm_t comm, size_t count, ddl_dtype_t dtype);
  * production: the skipped rank's data is not reduced. */
 ddl_result_t ddl_debug_skip_rank(ddl_comm_t comm, int rank);
 
+/* Test hook: connect nranks communicators that all live in THIS process on ONE GPU
+ * (comms[r] = rank r's handle from ddl_init, same dims/max_bytes), without cudaIpc: peers'
+ * workspaces are addressed directly.  Each rank's calls then run the multi-process kernel
+ * path (per-rank launches on the caller's streams, .sys-scope flags, zero-copy and staged
+ * buffers) with the ranks' kernels co-resident on one GPU (CTA budget divided by nranks). */
+ddl_result_t ddl_debug_connect_local(ddl_comm_t* comms, int nranks);
+
 /* Collective teardown: every rank must have finished all calls (host barrier first).
  * Unmaps peers, frees the workspace, destroys the handle.  NULL is a no-op. */
 ddl_result_t ddl_finalize(ddl_comm_t comm);

@@ -233,232 +233,12 @@ __device__ __forceinline__ Span slice_span(const KParams& p, int b) {
   return s;
 }
 
-// ------------------------------------------------------------------------ copies
-// Copy this CTA's slice of block b from src to dst (same element offsets; the source may
-// be shifted by src_shift elements, for the allgather copy-in of a one-block send buffer).
-template <typename T, bool VEC>
-__device__ __forceinline__ void copy_block(const KParams& p, const char* src, char* dst, int b,
-                                           int64_t src_shift) {
-  constexpr int W = VEC ? Tr<T>::W : 1;
-  constexpr int U = 8;
-  const Span s = slice_span<W>(p, b);
-  const char* ps = src + ((int64_t)s.e0 - src_shift) * (int64_t)sizeof(T);
-  char* pd = dst + s.e0 * sizeof(T);
-  for (uint32_t j0 = threadIdx.x; j0 < s.nvec; j0 += U * blockDim.x) {
-    uint4 v[U];
-    uint32_t e1[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t j = j0 + u * blockDim.x;
-      if (j < s.nvec) {
-        if constexpr (VEC) v[u] = ld_vec(ps + (size_t)j * 16);
-        else e1[u] = ld_elem<T>(ps + (size_t)j * sizeof(T));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t j = j0 + u * blockDim.x;
-      if (j < s.nvec) {
-        if constexpr (VEC) st_vec(pd + (size_t)j * 16, v[u]);
-        else st_elem<T>(pd + (size_t)j * sizeof(T), e1[u]);
-      }
-    }
-  }
-  if (threadIdx.x < s.rem) {
-    const size_t o = ((size_t)s.nvec * W + threadIdx.x) * sizeof(T);
-    st_elem<T>(pd + o, ld_elem<T>(ps + o));
-  }
-}
-
-// ------------------------------------------------------------------------ RS phase (K1 + K3)
-// For each block b in A_{d+1}(me):  y = ((x_{m_0} + x_{m_1}) + ...) + x_{m_{g-1}}  (ascending
-// coordinate v of the group-d member), [ * fl32(1/P) in the last phase for avg ], cast, store.
-// G > 0: group size known at compile time (all loads of an item issued together);
-// G == 0: any g, loads issued in chunks of 8 members.
-template <typename T, bool VEC, int G>
-__device__ __forceinline__ void rs_phase(const KParams& p, int me, int d, bool first, bool last) {
-  using A = typename Tr<T>::Acc;
-  constexpr int W = VEC ? Tr<T>::W : 1;
-  constexpr int NA = W;
-  constexpr int GC = G > 0 ? G : 8;
-  constexpr int U = G > 0 ? (4 / G > 0 ? 4 / G : 1) : 1;  // <= 4 loads in flight per thread (no spills at 128 regs)
-  constexpr int ES = VEC ? 16 : (int)sizeof(T);
-  const Topo& t = p.t;
-  const int g = G > 0 ? G : t.g[d];
-  const bool do_scale = last && p.op == kAvg;
-  const int nb = nblocks(t, d + 1);
-  const void* const* srcs = first ? p.in : (const void* const*)p.work;
-  char* dstbase = static_cast<char*>(last ? p.out[me] : p.work[me]);
-  int mem[GC];
-  if constexpr (G > 0) {
-#pragma unroll
-    for (int v = 0; v < G; ++v) mem[v] = member(t, me, d, v);
-  }
-
-  for (int bi = 0; bi < nb; ++bi) {
-    const int b = block_of(t, me, d + 1, bi);
-    const Span s = slice_span<W>(p, b);
-    const size_t boff = s.e0 * sizeof(T);
-    char* pd = dstbase + boff;
-    for (uint32_t j0 = threadIdx.x; j0 < s.nvec; j0 += U * blockDim.x) {
-      A acc[U][NA];
-      for (int v0 = 0; v0 < g; v0 += GC) {
-        if constexpr (G == 0) {
-#pragma unroll
-          for (int v = 0; v < GC; ++v) mem[v] = v0 + v < g ? member(t, me, d, v0 + v) : me;
-        }
-        uint4 raw[U][GC];
-        uint32_t raw1[U][GC];
-#pragma unroll
-        for (int v = 0; v < GC; ++v) {
-          if (G == 0 && v0 + v >= g) break;
-          const char* ps = static_cast<const char*>(srcs[mem[v]]) + boff;
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t j = j0 + u * blockDim.x;
-            if (j < s.nvec) {
-              if constexpr (VEC) raw[u][v] = ld_vec(ps + (size_t)j * ES);
-              else raw1[u][v] = ld_elem<T>(ps + (size_t)j * ES);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-          for (int v = 0; v < GC; ++v) {
-            if (G == 0 && v0 + v >= g) break;
-            A x[NA];
-            if constexpr (VEC) unpack<T>(raw[u][v], x);
-            else x[0] = Tr<T>::to(raw1[u][v]);
-#pragma unroll
-            for (int i = 0; i < NA; ++i) acc[u][i] = (v0 + v == 0) ? x[i] : Tr<T>::add(acc[u][i], x[i]);
-          }
-          if (v0 + GC >= g) {  // fold complete: epilogue (K3) and store
-            const uint32_t j = j0 + u * blockDim.x;
-            if (j < s.nvec) {
-              if (do_scale) {
-#pragma unroll
-                for (int i = 0; i < NA; ++i) acc[u][i] = Tr<T>::mul(acc[u][i], p.scale);
-              }
-              if constexpr (VEC) st_vec(pd + (size_t)j * ES, pack<T>(acc[u]));
-              else st_elem<T>(pd + (size_t)j * ES, Tr<T>::from(acc[u][0]));
-            }
-          }
-        }
-      }
-    }
-    if (threadIdx.x < s.rem) {  // ragged end of the vector, element by element
-      const size_t o = boff + ((size_t)s.nvec * W + threadIdx.x) * sizeof(T);
-      A a = 0;
-      for (int v = 0; v < g; ++v) {
-        const A x = Tr<T>::to(ld_elem<T>(static_cast<const char*>(srcs[member(t, me, d, v)]) + o));
-        a = v == 0 ? x : Tr<T>::add(a, x);
-      }
-      if (do_scale) a = Tr<T>::mul(a, p.scale);
-      st_elem<T>(dstbase + o, Tr<T>::from(a));
-    }
-  }
-}
-
-template <typename T, bool VEC>
-__device__ __forceinline__ void rs_dispatch(const KParams& p, int me, int d, bool first, bool last) {
-  switch (p.t.g[d]) {
-    case 2: rs_phase<T, VEC, 2>(p, me, d, first, last); break;
-    case 3: rs_phase<T, VEC, 3>(p, me, d, first, last); break;
-    case 4: rs_phase<T, VEC, 4>(p, me, d, first, last); break;
-    case 8: rs_phase<T, VEC, 8>(p, me, d, first, last); break;
-    default: rs_phase<T, VEC, 0>(p, me, d, first, last); break;
-  }
-}
-
-// ------------------------------------------------------------------------ AG phase (K2)
-// For every group-d peer m_v (v != c_d(me)) and every block b in A_{d+1}(m_v): copy this
-// CTA's slice of block b from work[m_v] to work[me].  Pure bit copy.
-template <typename T, bool VEC>
-__device__ __forceinline__ void ag_phase(const KParams& p, int me, int d) {
-  const Topo& t = p.t;
-  const int c = coord(t, me, d);
-  const int nb = nblocks(t, d + 1);
-  for (int v = 0; v < t.g[d]; ++v) {
-    if (v == c) continue;
-    const int m = member(t, me, d, v);
-    for (int bi = 0; bi < nb; ++bi)
-      copy_block<T, VEC>(p, static_cast<const char*>(p.work[m]), static_cast<char*>(p.work[me]),
-                         block_of(t, m, d + 1, bi), 0);
-  }
-}
-
-// ------------------------------------------------------------------------ TMA-staged phases
-// The 16-byte-vector path of every phase (RS, AG, copy-in/out) runs through a kStages-deep
-// shared-memory ring filled by bulk asynchronous copies (cp.async.bulk, the TMA engine's
-// linear mode) from local or peer-mapped global memory.  One elected thread issues the
-// copies and arms an mbarrier per stage with the expected byte count; all 512 threads wait
-// on it, fold the g staged segments in ascending member order from shared memory, and
-// store the result with 16-byte st.global.  Bytes in flight per SM = CTAs/SM * kStages *
-// kStageBytes (default 2 * 2 * 48 KB), independent of registers -- the latency-hiding budget
-// HBM and NVLink need (round-1 ncu: the register-staged path sat at 16 warps/SM and 48% of
-// DRAM peak).  Defaults picked by the stage/size sweep in profiles/r01_tma_sweep.txt.
-#ifndef DDL_TMA_STAGES
-#define DDL_TMA_STAGES 2
-#endif
-#ifndef DDL_TMA_STAGE_KB
-#define DDL_TMA_STAGE_KB 48
-#endif
-#ifndef DDL_TMA_MINBLOCKS
-#define DDL_TMA_MINBLOCKS 2
-#endif
-constexpr int kStages = DDL_TMA_STAGES;
-constexpr uint32_t kStageBytes = DDL_TMA_STAGE_KB * 1024;
-constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t);
-
-__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
-  return (uint32_t)__cvta_generic_to_shared(ptr);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "DDL_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra DDL_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-// Make data that generic-proxy stores (this CTA's or a peer's, acquired through a device
-// barrier) visible to this thread's subsequent async-proxy (bulk copy) reads.
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-struct Pipe {
-  char* smem;
-  uint64_t* bar;
-  uint32_t seq;  // chunks consumed so far by this CTA (identical in every thread)
-};
-
-__device__ __forceinline__ void pipe_init(Pipe& pp) {
-  extern __shared__ __align__(128) char dsmem[];
-  pp.smem = dsmem;
-  pp.bar = reinterpret_cast<uint64_t*>(dsmem + (size_t)kStages * kStageBytes);
-  pp.seq = 0;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&pp.bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-}
-
+// ------------------------------------------------------------------------ phase units
+// A phase is a list of "units": this CTA's slice of one block, read from g sources (RS: the
+// group-d members, ascending coordinate) or one source (AG: the peer that owns the block;
+// copy-in/out: the user buffer / the work buffer), written to one destination at the same
+// element offsets.  Both data paths below (register-staged and TMA-staged) walk the same
+// unit list, kept in a small shared-memory table per phase.
 enum PhaseKind : int { kPhRS = 0, kPhAG = 1, kPhCin = 2, kPhCinOwn = 3, kPhCout = 4 };
 
 struct PhaseCtx {
@@ -533,29 +313,247 @@ __device__ __forceinline__ char* dst_base(const KParams& p, int me, const PhaseC
 }
 
 struct UnitDesc {
-  uint64_t e0;     // first element of this CTA's slice of the unit's block
-  uint32_t bytes;  // whole 16-byte vectors, in bytes
-  uint32_t rem;    // ragged elements after them
-  int srank;       // AG: source rank
-  int pad;
+  uint64_t e0;      // first element of this CTA's slice of the unit's block
+  uint32_t bytes;   // whole W-element items, in bytes
+  uint32_t rem;     // ragged elements after them
+  const char* src;  // copies (AG / copy-in / copy-out): the unit's source buffer base
 };
+
+// ------------------------------------------------------------------------ register-staged phases
+// Every thread walks the flattened (unit, vector) item list of the phase with U items in
+// flight: all loads of its U items (g each for RS) are issued before any fold/store, so a
+// phase of many small units costs one memory round trip, not one per unit.  PATH 0 runs the
+// same code element-wise (unaligned reduce-scatter / allgather layouts).
+template <typename T, bool VEC, int G>
+__device__ __forceinline__ void ldg_phase_g(const KParams& p, const PhaseCtx& x, char* dst, const UnitDesc* units,
+                                            const uint32_t* pref, const char* const* srcs) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = VEC ? Tr<T>::W : 1;
+  constexpr int GC = G > 0 ? G : 8;                                  // loads per item per round
+  constexpr int U = G == 1 ? 8 : (G > 0 && 4 / G > 0 ? 4 / G : 1);  // items per thread per iteration
+  const bool rs = G != 1;
+  const int g = rs ? x.g : 1;
+  const bool do_scale = rs && x.last && p.op == kAvg;
+  const char* sreg[GC];
+  if constexpr (G > 1) {
+#pragma unroll
+    for (int v = 0; v < G; ++v) sreg[v] = srcs[v];
+  }
+  const uint32_t total = pref[x.nunits];
+  int k = 0;  // unit cursor (items only increase along a thread's walk)
+  for (uint32_t base = threadIdx.x; base < total; base += U * blockDim.x) {
+    size_t off[U];  // byte offset of the item (same in sources and destination)
+    const char* us[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t it = base + u * blockDim.x;
+      off[u] = ~(size_t)0;
+      if (it < total) {
+        while (it >= pref[k + 1]) ++k;
+        off[u] = (units[k].e0 + (size_t)(it - pref[k]) * W) * sizeof(T);
+        us[u] = units[k].src;
+      }
+    }
+    A acc[U][W];
+    for (int v0 = 0; v0 < g; v0 += GC) {
+      if constexpr (G == 0) {
+#pragma unroll
+        for (int v = 0; v < GC; ++v) sreg[v] = v0 + v < g ? srcs[v0 + v] : nullptr;
+      }
+      uint4 raw[U][GC];
+      uint32_t raw1[U][GC];
+#pragma unroll
+      for (int v = 0; v < GC; ++v) {
+        if (v0 + v >= g) break;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (off[u] == ~(size_t)0) continue;
+          const char* ps = (G == 1 ? us[u] : sreg[v]) + off[u];
+          if constexpr (VEC) raw[u][v] = ld_vec(ps);
+          else raw1[u][v] = ld_elem<T>(ps);
+        }
+      }
+      if constexpr (G == 1) {  // copy: store the raw bits
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (off[u] == ~(size_t)0) continue;
+          if constexpr (VEC) st_vec(dst + off[u], raw[u][0]);
+          else st_elem<T>(dst + off[u], raw1[u][0]);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int v = 0; v < GC; ++v) {
+            if (v0 + v >= g) break;
+            A y[W];
+            if constexpr (VEC) unpack<T>(raw[u][v], y);
+            else y[0] = Tr<T>::to(raw1[u][v]);
+#pragma unroll
+            for (int i = 0; i < W; ++i) acc[u][i] = (v0 + v == 0) ? y[i] : Tr<T>::add(acc[u][i], y[i]);
+          }
+          if (v0 + GC >= g && off[u] != ~(size_t)0) {  // fold complete: epilogue (K3) and store
+            if (do_scale) {
+#pragma unroll
+              for (int i = 0; i < W; ++i) acc[u][i] = Tr<T>::mul(acc[u][i], p.scale);
+            }
+            if constexpr (VEC) st_vec(dst + off[u], pack<T>(acc[u]));
+            else st_elem<T>(dst + off[u], Tr<T>::from(acc[u][0]));
+          }
+        }
+      }
+    }
+  }
+}
+
+// Fill the phase's unit table (and RS source table); shared by both data paths.
+template <typename T, int W>
+__device__ __forceinline__ void fill_units(const KParams& p, int me, const PhaseCtx& x, UnitDesc* units,
+                                           const char** srcs, uint32_t* pref) {
+  __syncthreads();  // the previous phase's readers of the tables are done
+  if ((int)threadIdx.x < x.nunits) {
+    int sr;
+    const Span sp = slice_span<W>(p, unit_block(p, me, x, threadIdx.x, &sr));
+    units[threadIdx.x] = UnitDesc{sp.e0, sp.nvec * (uint32_t)(W * sizeof(T)), sp.rem,
+                                  x.kind == kPhRS ? nullptr : src_base<T>(p, me, x, 0, sr)};
+  }
+  if (x.kind == kPhRS && (int)threadIdx.x < x.g) srcs[threadIdx.x] = src_base<T>(p, me, x, threadIdx.x, me);
+  __syncthreads();
+  if (threadIdx.x == 0 && pref) {
+    uint32_t acc = 0;
+    for (int u = 0; u < x.nunits; ++u) {
+      pref[u] = acc;
+      acc += units[u].bytes / (uint32_t)(W * sizeof(T));
+    }
+    pref[x.nunits] = acc;
+  }
+  __syncthreads();
+}
+
+// ragged remainders (< 16 B where a slice is cut by n), element by element
+template <typename T>
+__device__ __forceinline__ void ragged_tails(const KParams& p, const PhaseCtx& x, char* dst, const UnitDesc* units,
+                                             const char* const* srcs) {
+  using A = typename Tr<T>::Acc;
+  const bool do_scale = x.kind == kPhRS && x.last && p.op == kAvg;
+  for (int u = 0; u < x.nunits; ++u) {
+    const UnitDesc ud = units[u];
+    if (threadIdx.x < ud.rem) {
+      const size_t o = (ud.e0 + (size_t)ud.bytes / sizeof(T) + threadIdx.x) * sizeof(T);
+      if (x.kind == kPhRS) {
+        A a = 0;
+        for (int v = 0; v < x.g; ++v) {
+          const A y = Tr<T>::to(ld_elem<T>(srcs[v] + o));
+          a = v == 0 ? y : Tr<T>::add(a, y);
+        }
+        if (do_scale) a = Tr<T>::mul(a, p.scale);
+        st_elem<T>(dst + o, Tr<T>::from(a));
+      } else {
+        st_elem<T>(dst + o, ld_elem<T>(ud.src + o));
+      }
+    }
+  }
+}
+
+template <typename T, bool VEC>
+__device__ void ldg_phase(const KParams& p, int me, const PhaseCtx& x) {
+  constexpr int W = VEC ? Tr<T>::W : 1;
+  __shared__ UnitDesc s_units[kMaxRanks];
+  __shared__ const char* s_srcs[kMaxRanks];
+  __shared__ uint32_t s_pref[kMaxRanks + 1];
+  fill_units<T, W>(p, me, x, s_units, s_srcs, s_pref);
+  char* dst = dst_base(p, me, x);
+  if (x.kind != kPhRS) ldg_phase_g<T, VEC, 1>(p, x, dst, s_units, s_pref, s_srcs);
+  else switch (x.g) {
+      case 2: ldg_phase_g<T, VEC, 2>(p, x, dst, s_units, s_pref, s_srcs); break;
+      case 4: ldg_phase_g<T, VEC, 4>(p, x, dst, s_units, s_pref, s_srcs); break;
+      case 8: ldg_phase_g<T, VEC, 8>(p, x, dst, s_units, s_pref, s_srcs); break;
+      default: ldg_phase_g<T, VEC, 0>(p, x, dst, s_units, s_pref, s_srcs); break;
+    }
+  ragged_tails<T>(p, x, dst, s_units, s_srcs);
+}
+
+// ------------------------------------------------------------------------ TMA-staged phases
+// The 16-byte-vector path of every phase (RS, AG, copy-in/out) runs through a kStages-deep
+// shared-memory ring filled by bulk asynchronous copies (cp.async.bulk, the TMA engine's
+// linear mode) from local or peer-mapped global memory.  One elected thread issues the
+// copies and arms an mbarrier per stage with the expected byte count; all 512 threads wait
+// on it, fold the g staged segments in ascending member order from shared memory, and
+// store the result with 16-byte st.global.  Bytes in flight per SM = CTAs/SM * kStages *
+// kStageBytes (default 2 * 2 * 48 KB), independent of registers -- the latency-hiding budget
+// HBM and NVLink need (round-1 ncu: the register-staged path sat at 16 warps/SM and 48% of
+// DRAM peak).  Defaults picked by the stage/size sweep in profiles/r01_tma_sweep.txt.
+#ifndef DDL_TMA_STAGES
+#define DDL_TMA_STAGES 2
+#endif
+#ifndef DDL_TMA_STAGE_KB
+#define DDL_TMA_STAGE_KB 48
+#endif
+#ifndef DDL_TMA_MINBLOCKS
+#define DDL_TMA_MINBLOCKS 2
+#endif
+constexpr int kStages = DDL_TMA_STAGES;
+constexpr uint32_t kStageBytes = DDL_TMA_STAGE_KB * 1024;
+constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DDL_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra DDL_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// Make data that generic-proxy stores (this CTA's or a peer's, acquired through a device
+// barrier) visible to this thread's subsequent async-proxy (bulk copy) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+struct Pipe {
+  char* smem;
+  uint64_t* bar;
+  uint32_t seq;  // chunks consumed so far by this CTA (identical in every thread)
+};
+
+__device__ __forceinline__ void pipe_init(Pipe& pp) {
+  extern __shared__ __align__(128) char dsmem[];
+  pp.smem = dsmem;
+  pp.bar = reinterpret_cast<uint64_t*>(dsmem + (size_t)kStages * kStageBytes);
+  pp.seq = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&pp.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
 
 template <typename T>
 __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp) {
   using A = typename Tr<T>::Acc;
   constexpr int W = Tr<T>::W;
   __shared__ UnitDesc s_units[kMaxRanks];
+  __shared__ const char* s_srcs[kMaxRanks];
   const uint32_t CB = (kStageBytes / (uint32_t)x.g) & ~15u;  // bytes per source per stage
   const bool do_scale = x.kind == kPhRS && x.last && p.op == kAvg;
   char* dst = dst_base(p, me, x);
-
-  __syncthreads();  // the previous phase's readers of s_units are done
-  if ((int)threadIdx.x < x.nunits) {
-    int sr;
-    const Span sp = slice_span<W>(p, unit_block(p, me, x, threadIdx.x, &sr));
-    s_units[threadIdx.x] = UnitDesc{sp.e0, sp.nvec * 16u, sp.rem, sr, 0};
-  }
-  __syncthreads();
+  fill_units<T, W>(p, me, x, s_units, s_srcs, nullptr);
   uint32_t total = 0;
   for (int u = 0; u < x.nunits; ++u) total += (s_units[u].bytes + CB - 1) / CB;
 
@@ -571,10 +569,13 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
     const uint32_t bytes = min(CB, ud.bytes - poff);
     const int st = (int)(sq % kStages);
     char* sbase = pp.smem + (size_t)st * kStageBytes;
+    const size_t go = ud.e0 * sizeof(T) + poff;
     mbar_arm(&pp.bar[st], bytes * (uint32_t)x.g);
-    for (int v = 0; v < x.g; ++v)
-      tma_load(sbase + (size_t)v * CB, src_base<T>(p, me, x, v, ud.srank) + ud.e0 * sizeof(T) + poff, bytes,
-               &pp.bar[st]);
+    if (x.kind == kPhRS) {
+      for (int v = 0; v < x.g; ++v) tma_load(sbase + (size_t)v * CB, s_srcs[v] + go, bytes, &pp.bar[st]);
+    } else {
+      tma_load(sbase, ud.src + go, bytes, &pp.bar[st]);
+    }
     poff += bytes;
   };
   if (threadIdx.x == 0 && total) {
@@ -621,25 +622,7 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
     if (threadIdx.x == 0 && j + kStages < total) issue(sq + kStages);
   }
   pp.seq += total;
-
-  // ragged remainders (< 16 B where a slice is cut by n), element by element
-  for (int u = 0; u < x.nunits; ++u) {
-    const UnitDesc ud = s_units[u];
-    if (threadIdx.x < ud.rem) {
-      const size_t o = (ud.e0 + (size_t)ud.bytes / sizeof(T) + threadIdx.x) * sizeof(T);
-      if (x.kind == kPhRS) {
-        A a = 0;
-        for (int v = 0; v < x.g; ++v) {
-          const A y = Tr<T>::to(ld_elem<T>(src_base<T>(p, me, x, v, ud.srank) + o));
-          a = v == 0 ? y : Tr<T>::add(a, y);
-        }
-        if (do_scale) a = Tr<T>::mul(a, p.scale);
-        st_elem<T>(dst + o, Tr<T>::from(a));
-      } else {
-        st_elem<T>(dst + o, ld_elem<T>(src_base<T>(p, me, x, 0, ud.srank) + o));
-      }
-    }
-  }
+  ragged_tails<T>(p, x, dst, s_units, s_srcs);
 }
 
 // ------------------------------------------------------------------------ the hierarchical kernel
@@ -658,39 +641,29 @@ __global__ void __launch_bounds__(kThreads, PATH == 2 ? DDL_TMA_MINBLOCKS : 1) d
   Pipe pp;
   if constexpr (PATH == 2) pipe_init(pp);
 
-  if (p.mode & kCinAll) {
-    if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhCin, 0, false, false), pp);
-    else
-      for (int b = 0; b < t.P; ++b)
-        copy_block<T, VEC>(p, static_cast<const char*>(p.cin[me]), static_cast<char*>(p.work[me]), b, 0);
-  }
-  if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T)) {
-    if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhCinOwn, 0, false, false), pp);
-    else
-      copy_block<T, VEC>(p, static_cast<const char*>(p.cin[me]), static_cast<char*>(p.work[me]), me,
-                         (int64_t)me * (int64_t)p.q);
-  }
+  auto run = [&](const PhaseCtx& x) {
+    if constexpr (PATH == 2) tma_phase<T>(p, me, x, pp);
+    else ldg_phase<T, VEC>(p, me, x);
+  };
+  if (p.mode & kCinAll) run(phase_ctx(p, me, kPhCin, 0, false, false));
+  if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T))
+    run(phase_ctx(p, me, kPhCinOwn, 0, false, false));
   if (p.mode & kRS) {
     for (int j = 0; j < L; ++j) {
       if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
-      if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1), pp);
-      else rs_dispatch<T, VEC>(p, me, t.live[j], j == 0, j == L - 1);
+      run(phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1));
     }
   }
   if (p.mode & kAG) {
     for (int jj = 0; jj < L; ++jj) {
       const int j = L + jj;
       if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
-      if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false), pp);
-      else ag_phase<T, VEC>(p, me, t.live[L - 1 - jj]);
+      run(phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false));
     }
   }
   if (p.mode & kCoutAll) {
     __syncthreads();
-    if constexpr (PATH == 2) tma_phase<T>(p, me, phase_ctx(p, me, kPhCout, 0, false, false), pp);
-    else
-      for (int b = 0; b < t.P; ++b)
-        copy_block<T, VEC>(p, static_cast<const char*>(p.work[me]), static_cast<char*>(p.cout[me]), b, 0);
+    run(phase_ctx(p, me, kPhCout, 0, false, false));
   }
   if (L > 0) dbarrier(p, me, 2 * L, barrier_npeers(t, 2 * L), e, group_peer(2 * L));
 }

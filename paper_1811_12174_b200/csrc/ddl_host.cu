@@ -92,7 +92,8 @@ struct ddl_comm {
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int skip_rank = -1;
   bool use_tma = true;
-  size_t tma_min_slice_bytes = 32 << 10;  // TMA path only when per-CTA slices are at least this big
+  int gpu_share = 1;  // ranks sharing this GPU (loopback: P; in-process test groups: P)
+  size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
 
   uint32_t* flags_of(int r) const {
     if (loopback) return reinterpret_cast<uint32_t*>(lb_flags + (size_t)r * flags_bytes);
@@ -190,7 +191,7 @@ const void* oneshot_fn_dt(ddl_dtype_t dt, int K) {
 // CTAs per rank that may be resident at once (loopback: all P ranks share the GPU).
 int cap_per_rank(const ddl_comm* c, const void* fn, size_t smem = 0) {
   int cap = blocks_per_sm(fn, smem) * c->num_sms;
-  if (c->loopback) cap /= c->P;
+  cap /= c->gpu_share;
   if (c->ctas_limit > 0 && c->ctas_limit < cap) cap = c->ctas_limit;
   if (cap > c->cmax) cap = c->cmax;
   return cap < 1 ? 1 : cap;
@@ -614,6 +615,26 @@ ddl_result_t ddl_debug_skip_rank(ddl_comm_t c, int rank) {
   return DDL_SUCCESS;
 }
 
+ddl_result_t ddl_debug_connect_local(ddl_comm_t* comms, int nranks) {
+  if (!comms || nranks < 1 || nranks > kMaxRanks) return DDL_ERR_INVALID_ARGUMENT;
+  for (int r = 0; r < nranks; ++r) {
+    const ddl_comm* c = comms[r];
+    if (!c || c->loopback || c->rank != r || c->P != nranks) return DDL_ERR_INVALID_ARGUMENT;
+    if (c->ndims != comms[0]->ndims || c->max_bytes != comms[0]->max_bytes || c->cmax != comms[0]->cmax ||
+        c->device != comms[0]->device)
+      return DDL_ERR_MISMATCH;
+    for (int d = 0; d < c->ndims; ++d)
+      if (c->dims[d] != comms[0]->dims[d]) return DDL_ERR_MISMATCH;
+  }
+  for (int r = 0; r < nranks; ++r) {
+    ddl_comm* c = comms[r];
+    for (int m = 0; m < nranks; ++m) c->peer_base[m] = m == r ? nullptr : comms[m]->alloc;
+    c->gpu_share = nranks;
+    c->connected = true;
+  }
+  return DDL_SUCCESS;
+}
+
 ddl_result_t ddl_finalize(ddl_comm_t c) {
   if (!c) return DDL_SUCCESS;
   cudaSetDevice(c->device);
@@ -635,6 +656,7 @@ ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, in
   ddl_comm* c = new (std::nothrow) ddl_comm();
   if (!c) return DDL_ERR_CUDA;
   c->loopback = true;
+  c->gpu_share = nranks;
   ddl_result_t r = common_init(c, nranks, dims, ndims, cuda_device);
   if (r != DDL_SUCCESS) {
     delete c;

@@ -75,6 +75,7 @@ def _load() -> ctypes.CDLL:
         "ddl_algo_for": (c_int, [c_void, c_size, c_int]),
         "ddl_ctas_for": (c_int, [c_void, c_size, c_int]),
         "ddl_debug_skip_rank": (c_int, [c_void, c_int]),
+        "ddl_debug_connect_local": (c_int, [pp, c_int]),
         "ddl_finalize": (c_int, [c_void]),
         "ddl_loopback_init": (c_int, [pp, c_int, ip, c_int, c_int]),
         "ddl_group_allreduce": (c_int, [c_void, pp, c_size, c_int, c_int, c_void]),
@@ -362,6 +363,80 @@ class Loopback:
             self.finalize()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------- in-process group (tests)
+class InProcessGroup:
+    """P ranks of the MULTI-PROCESS code path inside one process on one GPU (test hook
+    ``ddl_debug_connect_local``: peers addressed directly instead of through cudaIpc).
+    Each rank's call is launched on its own stream; the P kernels run concurrently."""
+
+    def __init__(self, nranks: int, dims=None, max_bytes: int = 64 << 20, device: int | None = None):
+        torch = _torch()
+        self.nranks = nranks
+        self.dims = parse_dims(dims, nranks)
+        self.device = torch.cuda.current_device() if device is None else device
+        hs = []
+        for r in range(nranks):
+            h = ctypes.c_void_p()
+            _check(_lib.ddl_init(ctypes.byref(h), r, nranks, _ints(self.dims), len(self.dims), self.device,
+                                 max_bytes), "ddl_init")
+            hs.append(h)
+        self.hs = hs
+        _check(_lib.ddl_debug_connect_local(_ptrs([h.value for h in hs]), nranks), "ddl_debug_connect_local")
+        self.streams = [torch.cuda.Stream() for _ in range(nranks)]
+        self.buf = []
+        for h in hs:
+            p = ctypes.c_void_p()
+            n = ctypes.c_size_t()
+            _check(_lib.ddl_buffer(h, ctypes.byref(p), ctypes.byref(n)), "ddl_buffer")
+            self.buf.append(_tensor_from_ptr(p.value, n.value, self.device))
+
+    def buffer(self, r: int, count: int, dtype, offset_bytes: int = 0):
+        esz = _torch().tensor([], dtype=dtype).element_size()
+        return self.buf[r][offset_bytes:offset_bytes + count * esz].view(dtype)
+
+    def _each(self, fn):
+        torch = _torch()
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        for r in range(self.nranks):
+            fn(r, self.streams[r].cuda_stream)
+        for s in self.streams:
+            cur.wait_stream(s)
+
+    def all_reduce(self, bufs, op: str = "sum"):
+        dt = DTYPE_CODES[dtype_name(bufs[0])]
+        self._each(lambda r, s: _check(_lib.ddl_allreduce(self.hs[r], bufs[r].data_ptr(), bufs[r].numel(), dt,
+                                                          OP_CODES[op], s), "ddl_allreduce"))
+        return bufs
+
+    def reduce_scatter(self, outs, inps, op: str = "sum"):
+        dt = DTYPE_CODES[dtype_name(outs[0])]
+        self._each(lambda r, s: _check(_lib.ddl_reduce_scatter(self.hs[r], inps[r].data_ptr(), outs[r].data_ptr(),
+                                                               outs[r].numel(), dt, OP_CODES[op], s),
+                                       "ddl_reduce_scatter"))
+        return outs
+
+    def all_gather(self, outs, inps):
+        dt = DTYPE_CODES[dtype_name(outs[0])]
+        self._each(lambda r, s: _check(_lib.ddl_allgather(self.hs[r], inps[r].data_ptr(), outs[r].data_ptr(),
+                                                          inps[r].numel(), dt, s), "ddl_allgather"))
+        return outs
+
+    def set_algo(self, algo: int, oneshot_max_bytes: int = 256 << 10) -> None:
+        for h in self.hs:
+            _check(_lib.ddl_set_algo(h, algo, oneshot_max_bytes), "ddl_set_algo")
+
+    def async_error(self) -> int:
+        return max(_lib.ddl_async_error(h) for h in self.hs)
+
+    def finalize(self) -> None:
+        _torch().cuda.synchronize()
+        for h in self.hs:
+            _lib.ddl_finalize(h)
+        self.hs = []
 
 
 # ---------------------------------------------------------------- K5

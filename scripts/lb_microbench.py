@@ -16,6 +16,7 @@ ap.add_argument("--op", default="avg")
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--algo", type=int, default=0)
 ap.add_argument("--oneshot-max", type=int, default=256 << 10)
+ap.add_argument("--graph", action="store_true", help="capture the timed calls in one CUDA graph (no host launch cost)")
 a = ap.parse_args()
 tdt = {"float32": torch.float32, "bfloat16": torch.bfloat16, "int32": torch.int32}[a.dtype]
 w = torch.tensor([], dtype=tdt).element_size()
@@ -28,11 +29,25 @@ for S in [int(x) for x in a.sizes.split(",")]:
     for _ in range(5):
         lb.all_reduce(bufs, a.op if a.dtype != "int32" else "sum")
     torch.cuda.synchronize()
+    op = a.op if a.dtype != "int32" else "sum"
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.iters):
-        lb.all_reduce(bufs, a.op if a.dtype != "int32" else "sum")
-    e1.record()
+    if a.graph:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(a.iters):
+                    lb.all_reduce(bufs, op)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+    else:
+        e0.record()
+        for _ in range(a.iters):
+            lb.all_reduce(bufs, op)
+        e1.record()
     torch.cuda.synchronize()
     assert lb.async_error() == 0
     us = e0.elapsed_time(e1) / a.iters * 1e3

@@ -1,0 +1,120 @@
+"""GPU parity of the MULTI-PROCESS kernel path on one B200: P communicators created with
+ddl_init (one per rank) in this process, connected with the ddl_debug_connect_local test
+hook instead of cudaIpc, each rank's call launched on its own stream so the P kernels run
+concurrently.  This exercises what loopback mode does not: per-rank launches, .sys-scope
+flags, the symmetric zero-copy buffer at equal offsets, the staged copy-in/copy-out path,
+and the staged reduce_scatter / allgather entry points.  Only the cudaIpc mapping itself
+(ddl_export_handle / ddl_connect) is not exercised on a 1-GPU box."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic_inputs as si
+from gpu_util import to_dev, to_host, same_bits, first_diff, TORCH
+from paper_1811_12174_b200 import ddl
+
+pytestmark = pytest.mark.gpu
+
+KIND = {"int32": "fullrange", "float32": "normal", "bfloat16": "normal"}
+_G = {}
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _short_timeout():
+    old = os.environ.get("DDL_TIMEOUT_MS")
+    os.environ["DDL_TIMEOUT_MS"] = "5000"
+    yield
+    for g in _G.values():
+        g.finalize()
+    _G.clear()
+    if old is None:
+        os.environ.pop("DDL_TIMEOUT_MS", None)
+    else:
+        os.environ["DDL_TIMEOUT_MS"] = old
+
+
+def group(P, dims):
+    key = (P, tuple(dims))
+    if key not in _G:
+        _G[key] = ddl.InProcessGroup(P, list(dims), max_bytes=64 << 20)
+    return _G[key]
+
+
+CASES = [(2, [2]), (4, [2, 2]), (4, [4]), (8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (6, [3, 2])]
+IDS = [f"P{P}-{'x'.join(map(str, d))}" for P, d in CASES]
+
+
+@pytest.mark.parametrize("P,dims", CASES, ids=IDS)
+@pytest.mark.parametrize("algo", [ddl.ALGO_HIER, ddl.ALGO_ONESHOT], ids=["hier", "oneshot"])
+def test_allreduce_zero_copy_and_staged(P, dims, algo):
+    g = group(P, dims)
+    g.set_algo(algo, 1 << 40)
+    for dtype in ("int32", "float32", "bfloat16"):
+        for op in (["sum"] if dtype == "int32" else ["sum", "avg"]):
+            for n in (1, 1000, 40_003, 300_001):
+                bufs = si.rank_buffers(dtype, KIND[dtype], n, P, seed=n + P)
+                want = oracle.allreduce(bufs, dims, dtype, op)
+                # zero-copy: inside the symmetric buffer, same offset on every rank
+                zc = [g.buffer(r, n, TORCH[dtype], offset_bytes=4096) for r in range(P)]
+                for r in range(P):
+                    zc[r].copy_(to_dev(bufs[r], dtype))
+                # staged: ordinary device tensors
+                st = [to_dev(b, dtype) for b in bufs]
+                g.all_reduce(zc, op)
+                g.all_reduce(st, op)
+                torch.cuda.synchronize()
+                assert g.async_error() == ddl.SUCCESS
+                for r in range(P):
+                    for name, t in (("zero-copy", zc[r]), ("staged", st[r])):
+                        got = to_host(t)
+                        assert same_bits(got, want[r]), (name, dims, dtype, op, n, r, first_diff(got, want[r]))
+
+
+@pytest.mark.parametrize("P,dims", CASES, ids=IDS)
+def test_reduce_scatter_allgather_staged(P, dims):
+    g = group(P, dims)
+    for recv in (96, 1001, 50_000):
+        for dtype in ("int32", "float32", "bfloat16"):
+            op = "sum" if dtype == "int32" else "avg"
+            bufs = si.rank_buffers(dtype, KIND[dtype], P * recv, P, seed=recv)
+            want = oracle.reduce_scatter(bufs, dims, dtype, op)
+            sends = [to_dev(b, dtype) for b in bufs]
+            recvs = [torch.empty(recv, dtype=TORCH[dtype], device="cuda") for _ in range(P)]
+            g.reduce_scatter(recvs, sends, op)
+            torch.cuda.synchronize()
+            for r in range(P):
+                got = to_host(recvs[r])
+                assert same_bits(got, want[r]), (recv, dtype, r, first_diff(got, want[r]))
+            blocks = si.rank_buffers(dtype, KIND[dtype], recv, P, seed=recv + 7)
+            wantg = oracle.allgather(blocks, dims, dtype)
+            sends = [to_dev(b, dtype) for b in blocks]
+            outs = [torch.empty(P * recv, dtype=TORCH[dtype], device="cuda") for _ in range(P)]
+            g.all_gather(outs, sends)
+            torch.cuda.synchronize()
+            for r in range(P):
+                assert same_bits(to_host(outs[r]), wantg[r]), (recv, dtype, r)
+    assert g.async_error() == ddl.SUCCESS
+
+
+def test_many_calls_mixed_paths():
+    """Epoch bookkeeping across calls that alternate algorithm, buffer kind and size."""
+    P, dims = 4, [2, 2]
+    g = group(P, dims)
+    g.set_algo(ddl.ALGO_AUTO, 64 << 10)
+    rng = np.random.Generator(np.random.PCG64(11))
+    for i in range(30):
+        n = int(rng.choice([5, 4000, 16_384, 100_000, 1_000_003]))
+        bufs = si.rank_buffers("int32", "fullrange", n, P, seed=i)
+        want = oracle.naive_sum(bufs, "int32")
+        if i % 2:
+            ts = [g.buffer(r, n, torch.int32) for r in range(P)]
+            for r in range(P):
+                ts[r].copy_(to_dev(bufs[r], "int32"))
+        else:
+            ts = [to_dev(b, "int32") for b in bufs]
+        g.all_reduce(ts)
+        torch.cuda.synchronize()
+        assert all(np.array_equal(to_host(t), want) for t in ts), (i, n)

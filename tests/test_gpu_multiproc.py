@@ -1,0 +1,80 @@
+"""Two real processes (torch.multiprocessing, gloo bootstrap), both on cuda:0: the complete
+multi-process bootstrap -- ddl_init, ddl_export_handle, all_gather_object of the cudaIpc
+handles, ddl_connect (cudaIpcOpenMemHandle) -- followed by zero-copy and staged
+all-reduces checked against the oracle.  On one GPU the two processes' kernels are
+time-sliced by the driver, so this proves the IPC mapping and the protocol, not speed."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, q):
+    import torch.distributed as dist
+    import oracle
+    import synthetic_inputs as si
+    from gpu_util import to_dev, to_host, same_bits
+    from paper_1811_12174_b200 import ddl
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), DDL_TIMEOUT_MS="20000")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    try:
+        comm = ddl.init([world], max_bytes=16 << 20)
+        for dtype, op in (("float32", "avg"), ("int32", "sum"), ("bfloat16", "sum")):
+            kind = "fullrange" if dtype == "int32" else "normal"
+            n = 50_003
+            bufs = si.rank_buffers(dtype, kind, n, world)
+            want = oracle.allreduce(bufs, [world], dtype, op)[rank]
+            zc = comm.buffer(n, to_dev(bufs[0][:1], dtype).dtype)
+            zc.copy_(to_dev(bufs[rank], dtype))
+            st = to_dev(bufs[rank], dtype)
+            comm.all_reduce(zc, op)
+            comm.all_reduce(st, op)
+            torch.cuda.synchronize()
+            res[dtype] = (same_bits(to_host(zc), want), same_bits(to_host(st), want))
+        res["err"] = comm.async_error()
+        comm.finalize()
+    except Exception as e:  # report, don't hang the parent
+        res["exc"] = repr(e)
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(240)
+def test_two_processes_ipc_one_gpu():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    try:
+        for _ in range(world):
+            r, res = q.get(timeout=200)
+            out[r] = res
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for r in range(world):
+        assert "exc" not in out[r], out[r]
+        assert out[r]["err"] == 0
+        for dtype in ("float32", "int32", "bfloat16"):
+            assert out[r][dtype] == (True, True), (r, dtype)
