@@ -166,7 +166,9 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
-    P, dims = 8, [4, 2]
+    # the ddl arm's configuration: N = 1 simulates the 8 ranks of 2x4; N > 1 runs N ranks
+    P = 8 if args.gpus == 1 else args.gpus
+    dims = oracle.parse_dims(args.dims or DIMS_FOR_N.get(args.gpus, str(args.gpus)))
     n = 1 << 20
     bufs = [si.resnet50_bucket(1, r)[:n] for r in range(P)]
     for _ in range(args.warmup):
@@ -179,11 +181,12 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "resnet50-grad-set sample: 1M fp32 x 8 simulated ranks, dims 2x4, avg",
-                       "dims": "2x4", "n_ranks": P},
+            "config": {"workload": f"resnet50-grad-set sample: 1M fp32 x {P} simulated ranks, dims "
+                                   + "x".join(map(str, dims[::-1])) + ", avg",
+                       "dims": "x".join(map(str, dims[::-1])), "n_ranks": P},
             "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": "each step: one oracle all-reduce of the first 1M elements of "
-                                       "ResNet-50 bucket 1 on 8 simulated ranks"},
+                                       f"ResNet-50 bucket 1 on {P} simulated ranks"},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -220,6 +223,8 @@ def run_loopback(args):
             step()
         torch.cuda.synchronize()
         assert lb.async_error() == ddl.SUCCESS
+        for b in range(nb):   # correctness gate: all virtual ranks bit-identical
+            assert all(torch.equal(bufs[b][0].view(torch.int32), t.view(torch.int32)) for t in bufs[b][1:])
         t_pad = time.perf_counter()
         while time.perf_counter() - t_pad < 0.3:   # keep the GPU busy so the sampler sees load clocks
             step()
@@ -313,8 +318,15 @@ def run_multi(args):
     from paper_1811_12174_b200 import ddl
 
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # DDL_BENCH_SAME_GPU=1: functional check of this code path with every rank on cuda:0
+    # (gloo bootstrap, no NCCL comparison; the kernels are time-sliced -- numbers meaningless)
+    same_gpu = os.environ.get("DDL_BENCH_SAME_GPU") == "1"
+    dev_idx = 0 if same_gpu else local
+    torch.cuda.set_device(dev_idx)
+    if same_gpu:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
     P = world
     dims = ddl.parse_dims(args.dims or DIMS_FOR_N.get(P, str(P)))
     host = resnet50_set(rank)
@@ -343,25 +355,32 @@ def run_multi(args):
         b.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
-        t = torch.tensor([a.elapsed_time(b) / steps], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([a.elapsed_time(b) / steps], device="cpu" if same_gpu else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)   # max over ranks
         return t.item()
 
     for _ in range(args.warmup):
         step()
-    with ClockSampler(local) as clk:
+    # correctness gate before timing: every rank holds bit-identical results
+    digest = torch.tensor([int(v.view(torch.int32).to(torch.int64).sum().item()) for v in views], dtype=torch.int64)
+    alld = [torch.zeros_like(digest) for _ in range(world)]
+    dist.all_gather(alld, digest.cuda() if not same_gpu else digest)
+    assert all(torch.equal(d.cpu(), alld[0].cpu()) for d in alld), "ranks disagree after all-reduce"
+    with ClockSampler(dev_idx) as clk:
         ms = timed(step, args.steps)
     assert comm.async_error() == ddl.SUCCESS
     busbw = S_total * 2 * (P - 1) / P / (ms * 1e-3) / 1e9
 
-    nccl_bufs = [torch.from_numpy(h).cuda() for h in host]
+    nccl_ms = None
+    if not same_gpu:
+        nccl_bufs = [torch.from_numpy(h).cuda() for h in host]
 
-    def nccl_step():
-        for t in nccl_bufs:
-            dist.all_reduce(t, op=dist.ReduceOp.AVG)
-    for _ in range(args.warmup):
-        nccl_step()
-    nccl_ms = timed(nccl_step, args.steps)
+        def nccl_step():
+            for t in nccl_bufs:
+                dist.all_reduce(t, op=dist.ReduceOp.AVG)
+        for _ in range(args.warmup):
+            nccl_step()
+        nccl_ms = timed(nccl_step, args.steps)
 
     # e2e: host gradients -> device (pinned H2D), all-reduce, reduced gradients -> host
     pinned = [torch.from_numpy(h).pin_memory() for h in host]
@@ -388,7 +407,8 @@ def run_multi(args):
                          "unit": "GB/s", "frac": busbw / NVLINK_MEASURED_PEER, "traffic": None,
                          "frac_of_nominal_900": busbw / NVLINK_NOMINAL,
                          "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)"},
-            "nccl": {"value": S_total * 2 * (P - 1) / P / (nccl_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": nccl_ms},
+            "nccl": None if nccl_ms is None else {"value": S_total * 2 * (P - 1) / P / (nccl_ms * 1e-3) / 1e9,
+                                                  "unit": "GB/s", "ms_per_step": nccl_ms},
             "e2e": {"value": S_total * 2 * (P - 1) / P / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": S_total, "d2h_bytes_per_step": S_total},
             "gpu_launches": len(sizes) * args.steps,
