@@ -155,6 +155,12 @@ int ddl_ctas_for(ddl_comm_t comm, size_t count, ddl_dtype_t dtype);
  * production: the skipped rank's data is not reduced. */
 ddl_result_t ddl_debug_skip_rank(ddl_comm_t comm, int rank);
 
+/* Debug: with DDL_TRACE=1 set at init, every CTA stamps %globaltimer (ns) at each phase
+ * boundary of each call (overwriting the previous call's stamps).  Copies the
+ * [nranks][cmax][40] uint64 timeline of the last call to host_out (synchronises).
+ * cmax = 4 * SM count.  DDL_ERR_UNSUPPORTED when tracing is off. */
+ddl_result_t ddl_debug_trace(ddl_comm_t comm, void* host_out, size_t bytes);
+
 /* Test hook: connect nranks communicators that all live in THIS process on ONE GPU
  * (comms[r] = rank r's handle from ddl_init, same dims/max_bytes), without cudaIpc: peers'
  * workspaces are addressed directly.  Each rank's calls then run the multi-process kernel

@@ -62,7 +62,18 @@ struct KParams {
   const void* cin[kMaxRanks];   // copy-in source of each rank
   void* cout[kMaxRanks];        // copy-out destination of each rank
   int mode;
+  uint64_t* trace;     // debug (DDL_TRACE=1): [P][cmax][kTraceEvents] globaltimer stamps, else null
 };
+constexpr int kTraceEvents = 40;
+
+// Debug timeline: thread 0 of each CTA stamps the global timer at event ev.
+__device__ __forceinline__ void trace_ev(const KParams& p, int me, int ev) {
+  if (p.trace && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[((size_t)me * p.cmax + blockIdx.x) * kTraceEvents + ev] = t;
+  }
+}
 
 struct LRParams {
   const void* in[kMaxLocalIn];
@@ -645,20 +656,28 @@ __global__ void __launch_bounds__(kThreads, PATH == 2 ? DDL_TMA_MINBLOCKS : 1) d
     if constexpr (PATH == 2) tma_phase<T>(p, me, x, pp);
     else ldg_phase<T, VEC>(p, me, x);
   };
+  // trace events: 0 start, 1 after copy-in, 2+2j after barrier j, 3+2j after the phase it gates,
+  // 2+2*(2L) after the end barrier
+  trace_ev(p, me, 0);
   if (p.mode & kCinAll) run(phase_ctx(p, me, kPhCin, 0, false, false));
   if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T))
     run(phase_ctx(p, me, kPhCinOwn, 0, false, false));
+  trace_ev(p, me, 1);
   if (p.mode & kRS) {
     for (int j = 0; j < L; ++j) {
       if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
+      trace_ev(p, me, 2 + 2 * j);
       run(phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1));
+      trace_ev(p, me, 3 + 2 * j);
     }
   }
   if (p.mode & kAG) {
     for (int jj = 0; jj < L; ++jj) {
       const int j = L + jj;
       if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
+      trace_ev(p, me, 2 + 2 * j);
       run(phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false));
+      trace_ev(p, me, 3 + 2 * j);
     }
   }
   if (p.mode & kCoutAll) {
@@ -666,6 +685,274 @@ __global__ void __launch_bounds__(kThreads, PATH == 2 ? DDL_TMA_MINBLOCKS : 1) d
     run(phase_ctx(p, me, kPhCout, 0, false, false));
   }
   if (L > 0) dbarrier(p, me, 2 * L, barrier_npeers(t, 2 * L), e, group_peer(2 * L));
+  trace_ev(p, me, 2 + 2 * (2 * L));
+}
+
+// ------------------------------------------------------------------------ rank-level, dynamic (PATH 3)
+// The same schedule, with the work of a phase shared DYNAMICALLY by all CTAs of a rank
+// (a ticket counter hands out chunks), and RANK-level barriers: when the last CTA of rank r
+// finishes phase j it signals the ranks that gate on it (barrier j+1's group, and r itself);
+// every CTA of those ranks waits for all of them before phase j+1.  Round-1 traces
+// (scripts/trace_call.py) showed per-CTA static slices finishing a phase up to 10-26 us
+// apart on one GPU, and every barrier waiting for the slowest CTA; dynamic chunks bound the
+// spread by one chunk.  All CTAs of all ranks must be co-resident (as for PATH 0-2).
+// MEASURED (round 1, loopback 8 ranks): 10-45% SLOWER than PATH 2 -- the spread is drain
+// latency of the last chunks, not load imbalance, and a rank-level barrier waits for the
+// slowest CTA of every member.  Kept behind DDL_DYN=1 (parity-tested), not the default.
+//
+// Rank state (in each rank's flag region, after the per-CTA area):
+//   [0] call epoch of this rank, then arrive[j] / work[j] counters per phase j (pre-phase =
+//   kPrePhase), then flags[slot][src]: src signalled slot with its epoch.
+constexpr int kNumSlots = 2 * kMaxDims + 1;
+constexpr int kPrePhase = kNumSlots;      // copy-in / nothing, before barrier 0
+constexpr int kPostPhase = kNumSlots + 1; // copy-out, after the end barrier
+constexpr int kRankStateWords = 16 + 2 * (kNumSlots + 2) + kNumSlots * kMaxRanks;
+
+__device__ __forceinline__ uint32_t* rank_state(const KParams& p, int r) {
+  return p.flags[r] + p.cmax + (size_t)kNumSlots * p.cmax * p.t.P;
+}
+__device__ __forceinline__ uint32_t* rs_arrive(uint32_t* rs, int j) { return rs + 16 + j; }
+__device__ __forceinline__ uint32_t* rs_work(uint32_t* rs, int j) { return rs + 16 + (kNumSlots + 2) + j; }
+__device__ __forceinline__ uint32_t* rs_flag(uint32_t* rs, int slot, int src) {
+  return rs + 16 + 2 * (kNumSlots + 2) + slot * kMaxRanks + src;
+}
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
+  return old;
+}
+
+// Barrier-slot peer lists: barrier j's group (j < 2L) or every group (j = 2L), plus r itself
+// (its own other CTAs wrote data this rank reads next).  Lane l < npeers+1.
+__device__ __forceinline__ int rank_barrier_member(const Topo& t, int me, int slot, int l) {
+  const int np = barrier_npeers(t, slot);
+  return l < np ? barrier_peer(t, me, slot, l) : me;
+}
+
+// Phase j of rank me done by this CTA: arrive; the last CTA resets the phase counters and
+// signals `slot` to its group + itself.
+__device__ __forceinline__ void rank_arrive(const KParams& p, int me, int j, int slot, uint32_t epoch) {
+  __syncthreads();  // this CTA's stores of phase j precede the release RMW below
+  if (threadIdx.x == 0) {
+    uint32_t* rs = rank_state(p, me);
+    const uint32_t old = atom_add_acq_rel_gpu(rs_arrive(rs, j), 1);
+    if (old == gridDim.x - 1) {  // last CTA of this rank: everything rank me wrote is visible to it
+      *rs_arrive(rs, j) = 0;
+      *rs_work(rs, j) = 0;
+      if (slot >= 0) {
+        const int np = barrier_npeers(p.t, slot);
+        for (int l = 0; l <= np; ++l) {
+          const int m = rank_barrier_member(p.t, me, slot, l);
+          st_release(rs_flag(rank_state(p, m), slot, me), epoch, p.loopback);
+        }
+      }
+    }
+  }
+}
+
+// Wait until every member of `slot` (group + me) has signalled it for this call.
+__device__ __forceinline__ bool rank_wait(const KParams& p, int me, int slot, uint32_t epoch) {
+  const int nw = barrier_npeers(p.t, slot) + 1;
+  int fail = 0;
+  if ((int)threadIdx.x < nw) {
+    const int m = rank_barrier_member(p.t, me, slot, threadIdx.x);
+    const uint32_t* f = rs_flag(rank_state(p, me), slot, m);
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
+    while ((int32_t)(ld_acquire(f, p.loopback) - epoch) < 0) {
+      if ((++spins & 1023u) == 0) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > p.timeout_ns) {
+          atomicExch(p.err, kErrTimeout);
+          fail = 1;
+          break;
+        }
+      }
+    }
+  }
+  return __syncthreads_or(fail) == 0;
+}
+
+struct ChunkDesc {
+  uint32_t unit;
+  uint32_t off;    // byte offset in the unit
+  uint32_t bytes;  // 0 = no more chunks for this CTA in this phase
+  uint32_t last;   // this chunk ends its unit (the unit's ragged remainder goes with it)
+};
+
+// One phase with chunks handed out by the rank's ticket counter.  Units are whole blocks.
+template <typename T>
+__device__ void dyn_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp, uint32_t* work) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = Tr<T>::W;
+  __shared__ UnitDesc s_units[kMaxRanks];
+  __shared__ const char* s_srcs[kMaxRanks];
+  __shared__ uint32_t s_cpref[kMaxRanks + 1];
+  __shared__ ChunkDesc s_desc[kStages];
+  const uint32_t CB = (kStageBytes / (uint32_t)x.g) & ~15u;
+  const bool do_scale = x.kind == kPhRS && x.last && p.op == kAvg;
+  char* dst = dst_base(p, me, x);
+
+  __syncthreads();  // previous phase's readers of the tables are done
+  if ((int)threadIdx.x < x.nunits) {
+    int sr;
+    const int b = unit_block(p, me, x, threadIdx.x, &sr);
+    const uint64_t e0 = (uint64_t)b * p.q;
+    const uint64_t len = e0 >= p.n ? 0 : (p.q < p.n - e0 ? p.q : p.n - e0);
+    const uint32_t nvec = (uint32_t)(len / W);
+    s_units[threadIdx.x] = UnitDesc{e0, nvec * 16u, (uint32_t)(len - (uint64_t)nvec * W),
+                                    x.kind == kPhRS ? nullptr : src_base<T>(p, me, x, 0, sr)};
+  }
+  if (x.kind == kPhRS && (int)threadIdx.x < x.g) s_srcs[threadIdx.x] = src_base<T>(p, me, x, threadIdx.x, me);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int u = 0; u < x.nunits; ++u) {
+      s_cpref[u] = acc;
+      // a unit with only a ragged remainder still gets one (empty) chunk to carry it
+      acc += s_units[u].bytes ? (s_units[u].bytes + CB - 1) / CB : (s_units[u].rem ? 1u : 0u);
+    }
+    s_cpref[x.nunits] = acc;
+  }
+  __syncthreads();
+  const uint32_t total = s_cpref[x.nunits];
+
+  // producer (thread 0): tickets -> stage descriptors + bulk loads
+  uint32_t ticket = 0;
+  bool done = false;
+  auto fill = [&](uint32_t sq) {
+    if (done) return;  // the terminator is already queued
+    const int st = (int)(sq % kStages);
+    ChunkDesc d{0, 0, 0, 0};
+    if (ticket < total) {
+      int u = 0;
+      while (ticket >= s_cpref[u + 1]) ++u;
+      const UnitDesc ud = s_units[u];
+      d.unit = u;
+      d.off = (ticket - s_cpref[u]) * CB;
+      d.bytes = ud.bytes > d.off ? min(CB, ud.bytes - d.off) : 0;
+      d.last = 0x80000000u | (ticket + 1 == s_cpref[u + 1] ? 1u : 0u);  // valid | ends its unit
+      s_desc[st] = d;
+      mbar_arm(&pp.bar[st], d.bytes * (uint32_t)x.g);
+      const size_t go = ud.e0 * sizeof(T) + d.off;
+      if (d.bytes) {
+        char* sb = pp.smem + (size_t)st * kStageBytes;
+        if (x.kind == kPhRS) {
+          for (int v = 0; v < x.g; ++v) tma_load(sb + (size_t)v * CB, s_srcs[v] + go, d.bytes, &pp.bar[st]);
+        } else {
+          tma_load(sb, ud.src + go, d.bytes, &pp.bar[st]);
+        }
+      }
+      ticket = atomicAdd(work, 1u);  // prefetch the next ticket
+    } else {
+      done = true;
+      s_desc[st] = d;  // terminator (no valid bit)
+      mbar_arm(&pp.bar[st], 0);
+    }
+  };
+  if (threadIdx.x == 0) {
+    fence_proxy_async_global();
+    ticket = atomicAdd(work, 1u);
+    for (int s = 0; s < kStages; ++s) {
+      fill(pp.seq + s);
+      if (done) break;
+    }
+  }
+
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t sq = pp.seq + k;
+    const int st = (int)(sq % kStages);
+    mbar_wait(&pp.bar[st], (sq / kStages) & 1u);
+    const ChunkDesc d = s_desc[st];
+    if (!(d.last & 0x80000000u)) {  // terminator: this CTA is done with the phase
+      pp.seq += k + 1;
+      break;
+    }
+    const UnitDesc ud = s_units[d.unit];
+    const char* sbase = pp.smem + (size_t)st * kStageBytes;
+    char* pd = dst + ud.e0 * sizeof(T) + d.off;
+    const uint32_t nv = d.bytes / 16u;
+    if (x.kind == kPhRS) {
+      for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+        A acc[W];
+        unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)i * 16), acc);
+        for (int v = 1; v < x.g; ++v) {
+          A y[W];
+          unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)v * CB + (size_t)i * 16), y);
+#pragma unroll
+          for (int q = 0; q < W; ++q) acc[q] = Tr<T>::add(acc[q], y[q]);
+        }
+        if (do_scale) {
+#pragma unroll
+          for (int q = 0; q < W; ++q) acc[q] = Tr<T>::mul(acc[q], p.scale);
+        }
+        st_vec(pd + (size_t)i * 16, pack<T>(acc));
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x)
+        st_vec(pd + (size_t)i * 16, *reinterpret_cast<const uint4*>(sbase + (size_t)i * 16));
+    }
+    if ((d.last & 1u) && threadIdx.x < ud.rem) {  // the unit's ragged remainder, element-wise
+      const size_t o = (ud.e0 + (size_t)ud.bytes / sizeof(T) + threadIdx.x) * sizeof(T);
+      if (x.kind == kPhRS) {
+        A a = 0;
+        for (int v = 0; v < x.g; ++v) {
+          const A y = Tr<T>::to(ld_elem<T>(s_srcs[v] + o));
+          a = v == 0 ? y : Tr<T>::add(a, y);
+        }
+        if (do_scale) a = Tr<T>::mul(a, p.scale);
+        st_elem<T>(dst + o, Tr<T>::from(a));
+      } else {
+        st_elem<T>(dst + o, ld_elem<T>(ud.src + o));
+      }
+    }
+    __syncthreads();  // every thread is done with stage st
+    if (threadIdx.x == 0) fill(sq + kStages);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_dyn_kernel(const __grid_constant__ KParams p) {
+  const int me = p.loopback ? (int)blockIdx.y : p.rank;
+  uint32_t* rs = rank_state(p, me);
+  __shared__ uint32_t s_e;
+  if (threadIdx.x == 0) s_e = *rs + 1;  // this rank's call number (CTA 0 stores it at the end)
+  __syncthreads();
+  const uint32_t e = s_e;
+  if (me == p.skip_rank) return;
+  const Topo& t = p.t;
+  const int L = t.nlive;
+  Pipe pp;
+  pipe_init(pp);
+  trace_ev(p, me, 0);
+  // pre-phase: copy-in (staged paths), then "my inputs are ready" = barrier 0 (or L for AG-only)
+  const int first_slot = (p.mode & kRS) ? 0 : L;
+  if (p.mode & kCinAll) dyn_phase<T>(p, me, phase_ctx(p, me, kPhCin, 0, false, false), pp, rs_work(rs, kPrePhase));
+  if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T))
+    dyn_phase<T>(p, me, phase_ctx(p, me, kPhCinOwn, 0, false, false), pp, rs_work(rs, kPrePhase));
+  rank_arrive(p, me, kPrePhase, first_slot, e);
+  trace_ev(p, me, 1);
+  // phases j = first_slot .. last; phase j follows barrier j, and its completion signals
+  // barrier j+1 (or the end barrier 2L after the last phase)
+  const int last_slot = (p.mode & kAG) ? 2 * L - 1 : L - 1;
+  for (int j = first_slot; j <= last_slot; ++j) {
+    if (!rank_wait(p, me, j, e)) return;
+    trace_ev(p, me, 2 + 2 * j);
+    const PhaseCtx x = j < L ? phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1)
+                             : phase_ctx(p, me, kPhAG, t.live[2 * L - 1 - j], false, false);
+    dyn_phase<T>(p, me, x, pp, rs_work(rs, j));
+    rank_arrive(p, me, j, j == last_slot ? 2 * L : j + 1, e);
+    trace_ev(p, me, 3 + 2 * j);
+  }
+  if (!rank_wait(p, me, 2 * L, e)) return;
+  if (p.mode & kCoutAll) {
+    dyn_phase<T>(p, me, phase_ctx(p, me, kPhCout, 0, false, false), pp, rs_work(rs, kPostPhase));
+    rank_arrive(p, me, kPostPhase, -1, e);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *rs = e;
+  trace_ev(p, me, 2 + 2 * (2 * L));
 }
 
 // ------------------------------------------------------------------------ one-shot (a9)

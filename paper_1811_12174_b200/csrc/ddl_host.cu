@@ -24,7 +24,6 @@ static_assert(DDL_MAX_DIMS == kMaxDims, "header / planner dims limit");
 namespace {
 
 constexpr uint32_t kMagic = 0xDD1A11EDu;
-constexpr int kNumSlots = 2 * kMaxDims + 1;
 
 thread_local std::string g_last_error;
 
@@ -92,7 +91,9 @@ struct ddl_comm {
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int skip_rank = -1;
   bool use_tma = true;
-  int gpu_share = 1;  // ranks sharing this GPU (loopback: P; in-process test groups: P)
+  bool use_dyn = false;  // DDL_DYN=1: rank-level barriers + dynamic chunks (measured slower)
+  int gpu_share = 1;
+  uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)  // ranks sharing this GPU (loopback: P; in-process test groups: P)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
 
   uint32_t* flags_of(int r) const {
@@ -126,6 +127,7 @@ void apply_env(ddl_comm* c) {
   c->min_slice_bytes = env_size("DDL_MIN_SLICE_BYTES", c->min_slice_bytes);
   c->ctas_limit = (int)env_size("DDL_CTAS", 0);
   c->use_tma = env_size("DDL_NO_TMA", 0) == 0;
+  c->use_dyn = env_size("DDL_DYN", 0) != 0;
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
@@ -145,9 +147,14 @@ ddl_result_t common_init(ddl_comm* c, int nranks, const int* dims, int ndims, in
   DDL_CUDA(cudaSetDevice(dev));
   DDL_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
   c->cmax = c->num_sms * 4;
-  const size_t words = (size_t)c->cmax * (1 + (size_t)kNumSlots * nranks);
+  const size_t words = (size_t)c->cmax * (1 + (size_t)kNumSlots * nranks) + kRankStateWords;
   c->flags_bytes = (words * 4 + 65535) / 65536 * 65536;
   apply_env(c);
+  if (env_size("DDL_TRACE", 0)) {
+    const size_t tb = (size_t)nranks * c->cmax * kTraceEvents * sizeof(uint64_t);
+    DDL_CUDA(cudaMalloc(&c->trace, tb));
+    DDL_CUDA(cudaMemset(c->trace, 0, tb));
+  }
   return DDL_SUCCESS;
 }
 
@@ -157,12 +164,14 @@ struct Plan {
   uint64_t slice = 0;
   int nctas = 0;
   bool vec = true;
-  int path = 2;  // hierarchical kernel variant: 0 element-wise, 1 register-staged, 2 TMA-staged
+  int path = 2;  // hierarchical kernel variant: 0 element-wise, 1 register-staged, 2 TMA-staged,
+                 // 3 TMA-staged with rank-level barriers and dynamic chunks
   bool oneshot = false;
 };
 
 template <typename T>
 const void* hier_fn(int path) {
+  if (path == 3) return (const void*)ddl_dyn_kernel<T>;
   if (path == 2) return (const void*)ddl_hier_kernel<T, 2>;
   return path == 1 ? (const void*)ddl_hier_kernel<T, 1> : (const void*)ddl_hier_kernel<T, 0>;
 }
@@ -181,7 +190,7 @@ const void* hier_fn_dt(ddl_dtype_t dt, int path) {
   if (dt == DDL_FLOAT32) return hier_fn<float>(path);
   return hier_fn<__nv_bfloat16>(path);
 }
-size_t hier_smem(int path) { return path == 2 ? kTmaSmem : 0; }
+size_t hier_smem(int path) { return path >= 2 ? kTmaSmem : 0; }
 const void* oneshot_fn_dt(ddl_dtype_t dt, int K) {
   if (dt == DDL_INT32) return oneshot_fn<int32_t>(K);
   if (dt == DDL_FLOAT32) return oneshot_fn<float>(K);
@@ -203,9 +212,9 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
   pl.vec = vec;
   const int w = elem_size(dt);
   const uint64_t W = vec ? 16 / w : 1;
-  pl.path = !vec ? 0 : (c->use_tma ? 2 : 1);
+  pl.path = !vec ? 0 : (c->use_tma ? (c->use_dyn ? 3 : 2) : 1);
   int cap = cap_per_rank(c, hier_fn_dt(dt, pl.path), hier_smem(pl.path));
-  if (pl.path == 2 && q * w < c->tma_min_slice_bytes * (uint64_t)cap) {
+  if (pl.path >= 2 && q * w < c->tma_min_slice_bytes * (uint64_t)cap) {
     // small per-CTA slices: the register-staged path has lower per-phase latency
     pl.path = 1;
     cap = cap_per_rank(c, hier_fn_dt(dt, 1), 0);
@@ -257,6 +266,7 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
   p.n = n;
   p.timeout_ns = c->timeout_ns;
   p.err = c->err;
+  p.trace = c->trace;
   for (int r = 0; r < c->P; ++r) p.flags[r] = c->flags_of(r);
   return p;
 }
@@ -615,6 +625,16 @@ ddl_result_t ddl_debug_skip_rank(ddl_comm_t c, int rank) {
   return DDL_SUCCESS;
 }
 
+ddl_result_t ddl_debug_trace(ddl_comm_t c, void* host_out, size_t bytes) {
+  if (!c || !host_out) return DDL_ERR_INVALID_ARGUMENT;
+  if (!c->trace) return DDL_ERR_UNSUPPORTED;
+  const size_t tb = (size_t)c->P * c->cmax * kTraceEvents * sizeof(uint64_t);
+  if (bytes < tb) return DDL_ERR_INVALID_ARGUMENT;
+  DDL_CUDA(cudaDeviceSynchronize());
+  DDL_CUDA(cudaMemcpy(host_out, c->trace, tb, cudaMemcpyDeviceToHost));
+  return DDL_SUCCESS;
+}
+
 ddl_result_t ddl_debug_connect_local(ddl_comm_t* comms, int nranks) {
   if (!comms || nranks < 1 || nranks > kMaxRanks) return DDL_ERR_INVALID_ARGUMENT;
   for (int r = 0; r < nranks; ++r) {
@@ -645,6 +665,7 @@ ddl_result_t ddl_finalize(ddl_comm_t c) {
   if (c->lb_flags) cudaFree(c->lb_flags);
   if (c->lb_ws) cudaFree(c->lb_ws);
   if (c->err) cudaFree(c->err);
+  if (c->trace) cudaFree(c->trace);
   delete c;
   return DDL_SUCCESS;
 }

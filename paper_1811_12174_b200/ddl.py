@@ -76,6 +76,7 @@ def _load() -> ctypes.CDLL:
         "ddl_ctas_for": (c_int, [c_void, c_size, c_int]),
         "ddl_debug_skip_rank": (c_int, [c_void, c_int]),
         "ddl_debug_connect_local": (c_int, [pp, c_int]),
+        "ddl_debug_trace": (c_int, [c_void, c_void, c_size]),
         "ddl_finalize": (c_int, [c_void]),
         "ddl_loopback_init": (c_int, [pp, c_int, ip, c_int, c_int]),
         "ddl_group_allreduce": (c_int, [c_void, pp, c_size, c_int, c_int, c_void]),
@@ -346,6 +347,15 @@ class Loopback:
 
     def ctas_for(self, count: int, dtype: str) -> int:
         return _lib.ddl_ctas_for(self.h, count, DTYPE_CODES[dtype])
+
+    def trace(self):
+        """[nranks][cmax][40] globaltimer stamps of the last call (DDL_TRACE=1 at init)."""
+        import numpy as np
+        torch = _torch()
+        cmax = 4 * torch.cuda.get_device_properties(self.device).multi_processor_count
+        out = np.zeros((self.nranks, cmax, 40), dtype=np.uint64)
+        _check(_lib.ddl_debug_trace(self.h, out.ctypes.data, out.nbytes), "ddl_debug_trace")
+        return out
 
     def debug_skip_rank(self, r: int) -> None:
         _check(_lib.ddl_debug_skip_rank(self.h, r), "ddl_debug_skip_rank")
