@@ -1,0 +1,49 @@
+"""Small loopback / in-process calls for compute-sanitizer (memcheck, racecheck, synccheck):
+every kernel variant once on tiny ragged inputs, results checked against the closed form."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1811_12174_b200 import ddl
+
+def check(bufs, want):
+    torch.cuda.synchronize()
+    assert all(bool((b == want).all()) for b in bufs)
+
+for P, dims in ((4, [2, 2]), (8, [4, 2]), (3, [3])):
+    lb = ddl.Loopback(P, dims)
+    for algo in (ddl.ALGO_HIER, ddl.ALGO_ONESHOT):
+        lb.set_algo(algo, 1 << 30)
+        for n in (1, 1003, 70_001):
+            for dt in (torch.float32, torch.int32, torch.bfloat16):
+                bufs = [torch.full((n,), r + 1, dtype=dt, device="cuda") for r in range(P)]
+                lb.all_reduce(bufs)
+                check(bufs, P * (P + 1) // 2)
+    # reduce-scatter / allgather, aligned and unaligned counts
+    for recv in (96, 101):
+        sends = [torch.full((P * recv,), r + 1, dtype=torch.float32, device="cuda") for r in range(P)]
+        outs = [torch.empty(recv, device="cuda") for _ in range(P)]
+        lb.reduce_scatter(outs, sends)
+        check(outs, P * (P + 1) // 2)
+        ins = [torch.full((recv,), r + 1.0, device="cuda") for r in range(P)]
+        g = [torch.empty(P * recv, device="cuda") for _ in range(P)]
+        lb.all_gather(g, ins)
+        torch.cuda.synchronize()
+        want = torch.arange(1, P + 1, device="cuda", dtype=torch.float32).repeat_interleave(recv)
+        assert all(torch.equal(x, want) for x in g)
+    lb.finalize()
+g = ddl.InProcessGroup(2, [2], max_bytes=1 << 20)
+for n in (5, 4099):
+    zc = [g.buffer(r, n, torch.float32) for r in range(2)]
+    for r in range(2):
+        zc[r].fill_(r + 1)
+    st = [torch.full((n,), r + 1.0, device="cuda") for r in range(2)]
+    g.all_reduce(zc)
+    g.all_reduce(st)
+    check(zc, 3)
+    check(st, 3)
+g.finalize()
+ins = [torch.full((1001,), float(j), device="cuda") for j in range(3)]
+out = torch.empty(1001, device="cuda")
+ddl.local_reduce(ins, out, 0.5)
+check([out], 1.5)
+print("sanitize_check ok")
