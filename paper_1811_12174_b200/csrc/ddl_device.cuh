@@ -211,16 +211,65 @@ __device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int
   return __syncthreads_or(fail) == 0;
 }
 
-__device__ __forceinline__ uint32_t next_epoch(const KParams& p, int me) {
+constexpr int kNumSlots = 2 * kMaxDims + 1;
+constexpr int kPrePhase = kNumSlots;      // copy-in / nothing, before barrier 0
+constexpr int kPostPhase = kNumSlots + 1; // copy-out, after the end barrier
+constexpr int kRankStateWords = 16 + 2 * (kNumSlots + 2) + kNumSlots * kMaxRanks;
+
+__device__ __forceinline__ uint32_t* rank_state(const KParams& p, int r) {
+  return p.flags[r] + p.cmax + (size_t)kNumSlots * p.cmax * p.t.P;
+}
+__device__ __forceinline__ uint32_t* rs_arrive(uint32_t* rs, int j) { return rs + 16 + j; }
+__device__ __forceinline__ uint32_t* rs_work(uint32_t* rs, int j) { return rs + 16 + (kNumSlots + 2) + j; }
+__device__ __forceinline__ uint32_t* rs_flag(uint32_t* rs, int slot, int src) {
+  return rs + 16 + 2 * (kNumSlots + 2) + slot * kMaxRanks + src;
+}
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
+  return old;
+}
+
+// Call epochs are per RANK (identical on every rank: all ranks make the same calls), so flags
+// written by any CTA of a rank compare against the same number whatever the CTA count of
+// each call.  Every CTA reads it at start; the last CTA to finish the call (end arrival)
+// advances it -- by then every CTA of the rank has read it.  The steal counters (PATH 4) are
+// reset there too.  Layout after the rank state:
+//   steal[0] end arrival, steal[16 + j*cmax + s] tickets, steal[16 + (kNumSlots + j)*cmax + s] done.
+__device__ __forceinline__ uint32_t* steal_base(const KParams& p, int r) { return rank_state(p, r) + kRankStateWords; }
+__device__ __forceinline__ uint32_t* steal_tick(const KParams& p, int r, int j) {
+  return steal_base(p, r) + 16 + (size_t)j * p.cmax;
+}
+__device__ __forceinline__ uint32_t* steal_done(const KParams& p, int r, int j) {
+  return steal_base(p, r) + 16 + (size_t)(kNumSlots + j) * p.cmax;
+}
+
+__device__ __forceinline__ uint32_t rank_epoch_begin(const KParams& p, int me) {
   __shared__ uint32_t s_epoch;
-  if (threadIdx.x == 0) {
-    uint32_t* ep = p.flags[me] + blockIdx.x;  // this CTA's call counter, local memory
-    const uint32_t e = *ep + 1;
-    *ep = e;
-    s_epoch = e;
-  }
+  if (threadIdx.x == 0) s_epoch = *rank_state(p, me) + 1;
   __syncthreads();
   return s_epoch;
+}
+
+__device__ __forceinline__ void rank_epoch_end(const KParams& p, int me, uint32_t e, int steal_phases) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* sb = steal_base(p, me);
+    const uint32_t old = atom_add_acq_rel_gpu(sb, 1);
+    s_last = (old == gridDim.x - 1);
+    if (s_last) *sb = 0;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (int j = 0; j < steal_phases; ++j)
+      for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+        steal_tick(p, me, j)[i] = 0;
+        steal_done(p, me, j)[i] = 0;
+      }
+    if (threadIdx.x == 0) *rank_state(p, me) = e;
+  }
 }
 
 // ------------------------------------------------------------------------ block/slice helpers
@@ -346,7 +395,8 @@ __device__ __forceinline__ void ldg_phase_g(const KParams& p, const PhaseCtx& x,
   using A = typename Tr<T>::Acc;
   constexpr int W = VEC ? Tr<T>::W : 1;
   constexpr int GC = G > 0 ? G : 8;                                  // loads per item per round
-  constexpr int U = G == 1 ? 8 : (G > 0 && 4 / G > 0 ? 4 / G : 1);  // items per thread per iteration
+  constexpr int GG = G > 0 ? G : 1;
+  constexpr int U = G == 1 ? 8 : (G > 0 && 4 / GG > 0 ? 4 / GG : 1);  // items per thread per iteration
   const bool rs = G != 1;
   const int g = rs ? x.g : 1;
   const bool do_scale = rs && x.last && p.op == kAvg;
@@ -641,32 +691,322 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
   ragged_tails<T>(p, x, dst, s_units, s_srcs);
 }
 
+// ------------------------------------------------------------------------ work stealing (PATH 4)
+// PATH 2's per-CTA slices and per-slice barriers, plus stealing: a CTA that has finished its
+// own slice of a phase takes chunks of other slices of the same rank (per-slice ticket
+// counters); every processed chunk is counted in its slice's done counter (release), and
+// the slice's owner, before signalling the next barrier for its slice, waits until all the
+// slice's chunks are done (acquire) -- whoever processed them.  Round-1 traces showed the
+// per-CTA phase time is SYSTEMATICALLY SM-dependent (same SMs 25% slower every call,
+// scripts/trace_variance.py), so static equal slices leave fast SMs idle at every barrier.
+// MEASURED (round 1): parity-green but 5-95% SLOWER than PATH 2 on 8-32 MB messages (the
+// per-chunk ticket atomics and the end-of-phase steal scan cost more than the imbalance
+// they remove).  Kept behind DDL_STEAL=1.
+
+// vector bytes / remainder of unit (block b) in slice s
+template <int W, typename T>
+__device__ __forceinline__ void slice_unit_span(const KParams& p, int b, int s, uint64_t* e0, uint32_t* vb,
+                                                uint32_t* rem) {
+  *vb = 0;
+  *rem = 0;
+  *e0 = 0;
+  const uint64_t cbase = (uint64_t)s * p.slice;
+  if (cbase >= p.q) return;
+  const uint64_t e = (uint64_t)b * p.q + cbase;
+  if (e >= p.n) return;
+  uint64_t len = p.q - cbase < p.slice ? p.q - cbase : p.slice;
+  if (len > p.n - e) len = p.n - e;
+  *e0 = e;
+  *vb = (uint32_t)(len / W) * 16u;
+  *rem = (uint32_t)(len % W);
+}
+__device__ __forceinline__ uint32_t unit_chunks(uint32_t vb, uint32_t rem, uint32_t CB) {
+  return vb ? (vb + CB - 1) / CB : (rem ? 1u : 0u);
+}
+template <typename T>
+__device__ uint32_t slice_chunks(const KParams& p, int me, const PhaseCtx& x, int s) {
+  constexpr int W = Tr<T>::W;
+  const uint32_t CB = (kStageBytes / (uint32_t)x.g) & ~15u;
+  uint32_t k = 0;
+  for (int u = 0; u < x.nunits; ++u) {
+    int sr;
+    uint64_t e0;
+    uint32_t vb, rem;
+    slice_unit_span<W, T>(p, unit_block(p, me, x, u, &sr), s, &e0, &vb, &rem);
+    k += unit_chunks(vb, rem, CB);
+  }
+  return k;
+}
+
+__device__ __forceinline__ void red_release_add(uint32_t* a, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+// The owner of slice blockIdx.x waits until every chunk of its slice in phase j is done.
+template <typename T>
+__device__ __forceinline__ bool own_slice_done(const KParams& p, int me, const PhaseCtx& x, int j) {
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) {
+    s_fail = 0;
+    const uint32_t K = slice_chunks<T>(p, me, x, blockIdx.x);
+    const uint32_t* d = steal_done(p, me, j) + blockIdx.x;
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
+    while (ld_acquire(d, true) < K) {
+      if ((++spins & 1023u) == 0) {
+        const uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > p.timeout_ns) {
+          atomicExch(p.err, kErrTimeout);
+          s_fail = 1;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return s_fail == 0;
+}
+
+struct StealDesc {
+  char* dst;       // destination of the chunk's first byte
+  uint32_t bytes;  // vector bytes (0: remainder-only chunk)
+  int slice;       // -1: terminator
+};
+
+template <typename T>
+__device__ void steal_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp, int j) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = Tr<T>::W;
+  __shared__ const char* s_srcs[kMaxRanks];
+  __shared__ const char* s_usrc[kMaxRanks];
+  __shared__ int s_blk[kMaxRanks];
+  __shared__ StealDesc s_desc[kStages];
+  // producer's (thread 0) view of the slice it is currently taking chunks from
+  __shared__ uint64_t s_e0[kMaxRanks];
+  __shared__ uint32_t s_vb[kMaxRanks], s_rem[kMaxRanks], s_kp[kMaxRanks + 1];
+  const uint32_t CB = (kStageBytes / (uint32_t)x.g) & ~15u;
+  const bool rs = x.kind == kPhRS;
+  const bool do_scale = rs && x.last && p.op == kAvg;
+  char* dst = dst_base(p, me, x);
+  uint32_t* tick = steal_tick(p, me, j);
+  uint32_t* done = steal_done(p, me, j);
+  const int C = gridDim.x;
+  const int own = blockIdx.x;
+
+  __syncthreads();  // previous phase's readers of the tables are done
+  if ((int)threadIdx.x < x.nunits) {
+    int sr;
+    s_blk[threadIdx.x] = unit_block(p, me, x, threadIdx.x, &sr);
+    s_usrc[threadIdx.x] = rs ? nullptr : src_base<T>(p, me, x, 0, sr);
+  }
+  if (rs && (int)threadIdx.x < x.g) s_srcs[threadIdx.x] = src_base<T>(p, me, x, threadIdx.x, me);
+  __syncthreads();
+
+  auto load_slice = [&](int sl) -> uint32_t {  // thread 0: span table of slice sl, returns its chunks
+    uint32_t k = 0;
+    for (int u = 0; u < x.nunits; ++u) {
+      uint64_t e0;
+      uint32_t vb, rem;
+      slice_unit_span<W, T>(p, s_blk[u], sl, &e0, &vb, &rem);
+      s_e0[u] = e0;
+      s_vb[u] = vb;
+      s_rem[u] = rem;
+      s_kp[u] = k;
+      k += unit_chunks(vb, rem, CB);
+    }
+    s_kp[x.nunits] = k;
+    return k;
+  };
+  int cur = own;
+  uint32_t kcur = 0, tkt = 0, kmax = 0;  // kmax: chunks of slice 0, the largest slice
+  bool finished = false;
+  auto next_chunk = [&](uint32_t* to) -> bool {
+    for (;;) {
+      if (cur < 0) return false;
+      if (tkt < kcur) {
+        *to = tkt;
+        tkt = atomicAdd(&tick[cur], 1u);  // prefetch the next ticket of this slice
+        return true;
+      }
+      // steal: probe the following slices 8 at a time (independent loads, one round trip)
+      // for one whose ticket counter is below the largest slice's chunk count
+      int found = -1;
+      while (found < 0) {
+        uint32_t tv[8];
+        int sl[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          sl[i] = (cur + 1 + i) % C;
+          tv[i] = *(volatile uint32_t*)&tick[sl[i]];
+        }
+        int adv = 8;
+#pragma unroll
+        for (int i = 7; i >= 0; --i)
+          if (sl[i] == own) adv = i;  // wrapped back to our own slice: scan complete
+        for (int i = 0; i < adv && found < 0; ++i)
+          if (tv[i] < kmax) found = sl[i];
+        if (found < 0) {
+          if (adv < 8) {
+            cur = -1;
+            return false;
+          }
+          cur = (cur + 8) % C;
+        }
+      }
+      cur = found;
+      kcur = load_slice(cur);
+      tkt = 0xffffffffu;  // no ticket of the new slice yet
+      if (kcur == 0 || *(volatile uint32_t*)&tick[cur] >= kcur) continue;
+      tkt = atomicAdd(&tick[cur], 1u);
+    }
+  };
+  auto fill = [&](uint32_t sq) {
+    if (finished) return;
+    const int st = (int)(sq % kStages);
+    uint32_t t;
+    if (!next_chunk(&t)) {
+      finished = true;
+      s_desc[st] = StealDesc{nullptr, 0, -1};
+      mbar_arm(&pp.bar[st], 0);
+      return;
+    }
+    int u = 0;
+    while (t >= s_kp[u + 1]) ++u;
+    const uint32_t k = s_kp[u + 1] - s_kp[u];
+    const uint32_t off = (t - s_kp[u]) * CB;
+    const uint32_t vb = s_vb[u], rem = s_rem[u];
+    const uint64_t e0 = s_e0[u];
+    const uint32_t bytes = vb > off ? min(CB, vb - off) : 0;
+    const size_t go = e0 * sizeof(T) + off;
+    if (t - s_kp[u] == k - 1 && rem) {  // the unit's ragged remainder, element-wise, by the producer
+      const size_t o0 = (e0 + vb / 16u * W) * sizeof(T);
+      for (uint32_t i = 0; i < rem; ++i) {
+        const size_t o = o0 + i * sizeof(T);
+        if (rs) {
+          A a = 0;
+          for (int v = 0; v < x.g; ++v) {
+            const A y = Tr<T>::to(ld_elem<T>(s_srcs[v] + o));
+            a = v == 0 ? y : Tr<T>::add(a, y);
+          }
+          if (do_scale) a = Tr<T>::mul(a, p.scale);
+          st_elem<T>(dst + o, Tr<T>::from(a));
+        } else {
+          st_elem<T>(dst + o, ld_elem<T>(s_usrc[u] + o));
+        }
+      }
+    }
+    s_desc[st] = StealDesc{dst + go, bytes, cur};
+    mbar_arm(&pp.bar[st], bytes * (uint32_t)x.g);
+    if (bytes) {
+      char* sb = pp.smem + (size_t)st * kStageBytes;
+      if (rs) {
+        for (int v = 0; v < x.g; ++v) tma_load(sb + (size_t)v * CB, s_srcs[v] + go, bytes, &pp.bar[st]);
+      } else {
+        tma_load(sb, s_usrc[u] + go, bytes, &pp.bar[st]);
+      }
+    }
+  };
+  if (threadIdx.x == 0) {
+    fence_proxy_async_global();
+    kmax = load_slice(0);
+    kcur = load_slice(own);
+    tkt = atomicAdd(&tick[own], 1u);
+    for (int st = 0; st < kStages; ++st) fill(pp.seq + st);
+  }
+
+  // consumers; thread 0 also counts the chunks it saw per slice and publishes each slice's
+  // count (one release per slice switch) -- the slice owner waits for the total
+  int cnt_slice = -1;
+  uint32_t cnt = 0;
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t sq = pp.seq + k;
+    const int st = (int)(sq % kStages);
+    mbar_wait(&pp.bar[st], (sq / kStages) & 1u);
+    const StealDesc d = s_desc[st];
+    if (d.slice < 0) {
+      pp.seq += k + 1;
+      break;
+    }
+    const char* sbase = pp.smem + (size_t)st * kStageBytes;
+    const uint32_t nv = d.bytes / 16u;
+    if (rs) {
+      for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+        A a[W];
+        unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)i * 16), a);
+        for (int v = 1; v < x.g; ++v) {
+          A y[W];
+          unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)v * CB + (size_t)i * 16), y);
+#pragma unroll
+          for (int q = 0; q < W; ++q) a[q] = Tr<T>::add(a[q], y[q]);
+        }
+        if (do_scale) {
+#pragma unroll
+          for (int q = 0; q < W; ++q) a[q] = Tr<T>::mul(a[q], p.scale);
+        }
+        st_vec(d.dst + (size_t)i * 16, pack<T>(a));
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x)
+        st_vec(d.dst + (size_t)i * 16, *reinterpret_cast<const uint4*>(sbase + (size_t)i * 16));
+    }
+    __syncthreads();  // stage st consumed; the chunk's stores precede any later release
+    if (threadIdx.x == 0) {
+      if (d.slice != cnt_slice) {
+        if (cnt) red_release_add(&done[cnt_slice], cnt);
+        cnt_slice = d.slice;
+        cnt = 0;
+      }
+      ++cnt;
+      fill(sq + kStages);
+    }
+  }
+  if (threadIdx.x == 0 && cnt) red_release_add(&done[cnt_slice], cnt);
+}
+
 // ------------------------------------------------------------------------ the hierarchical kernel
 // PATH: 0 = element-wise loads (unaligned RS/AG layouts), 1 = 16-byte register-staged
-// loads, 2 = 16-byte TMA-staged (default).
+// loads, 2 = 16-byte TMA-staged (default), 4 = TMA-staged with work stealing.
 template <typename T, int PATH>
-__global__ void __launch_bounds__(kThreads, PATH == 2 ? DDL_TMA_MINBLOCKS : 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
   constexpr bool VEC = PATH >= 1;
+  constexpr bool TMA = PATH >= 2;
+  constexpr bool STEAL = PATH == 4;
   const int me = p.loopback ? (int)blockIdx.y : p.rank;
-  const uint32_t e = next_epoch(p, me);
+  const uint32_t e = rank_epoch_begin(p, me);
   if (me == p.skip_rank) return;
   const Topo& t = p.t;
   const int L = t.nlive;
   const int me_ = me;
   auto group_peer = [&](int j) { return [&p, me_, j](int l) { return barrier_peer(p.t, me_, j, l); }; };
   Pipe pp;
-  if constexpr (PATH == 2) pipe_init(pp);
+  if constexpr (TMA) pipe_init(pp);
 
-  auto run = [&](const PhaseCtx& x) {
-    if constexpr (PATH == 2) tma_phase<T>(p, me, x, pp);
+  auto run = [&](const PhaseCtx& x, int j) {
+    if constexpr (STEAL) {
+      if (x.kind == kPhRS || x.kind == kPhAG) {
+        steal_phase<T>(p, me, x, pp, j);
+        return;
+      }
+    }
+    if constexpr (TMA) tma_phase<T>(p, me, x, pp);
     else ldg_phase<T, VEC>(p, me, x);
+  };
+  // STEAL: before signalling barrier j, wait until this CTA's slice of phase j-1 is done
+  PhaseCtx prev{};
+  bool have_prev = false;
+  auto settle = [&](int j) -> bool {
+    if constexpr (STEAL) {
+      if (have_prev) return own_slice_done<T>(p, me, prev, j - 1);
+    }
+    return true;
   };
   // trace events: 0 start, 1 after copy-in, 2+2j after barrier j, 3+2j after the phase it gates,
   // 2+2*(2L) after the end barrier
   trace_ev(p, me, 0);
-  if (p.mode & kCinAll) run(phase_ctx(p, me, kPhCin, 0, false, false));
+  if (p.mode & kCinAll) run(phase_ctx(p, me, kPhCin, 0, false, false), -1);
   if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T))
-    run(phase_ctx(p, me, kPhCinOwn, 0, false, false));
+    run(phase_ctx(p, me, kPhCinOwn, 0, false, false), -1);
   trace_ev(p, me, 1);
   // Loopback: every virtual rank's inputs are ready when the launch starts and nothing can
   // touch any buffer before the whole launch ends (stream order), so the start barrier
@@ -674,27 +1014,39 @@ __global__ void __launch_bounds__(kThreads, PATH == 2 ? DDL_TMA_MINBLOCKS : 1) d
   const bool implied_start = p.loopback && !(p.mode & (kCinAll | kCinOwn));
   if (p.mode & kRS) {
     for (int j = 0; j < L; ++j) {
+      if (!settle(j)) return;
       if (!(j == 0 && implied_start) && !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
       trace_ev(p, me, 2 + 2 * j);
-      run(phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1));
+      prev = phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1);
+      run(prev, j);
+      have_prev = true;
       trace_ev(p, me, 3 + 2 * j);
     }
   }
   if (p.mode & kAG) {
     for (int jj = 0; jj < L; ++jj) {
       const int j = L + jj;
+      if (!settle(j)) return;
       if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
       trace_ev(p, me, 2 + 2 * j);
-      run(phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false));
+      prev = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false);
+      run(prev, j);
+      have_prev = true;
       trace_ev(p, me, 3 + 2 * j);
     }
   }
+  const int last_phase = (p.mode & kAG) ? 2 * L - 1 : L - 1;
   if (p.mode & kCoutAll) {
+    if (!settle(last_phase + 1)) return;
     __syncthreads();
-    run(phase_ctx(p, me, kPhCout, 0, false, false));
+    run(phase_ctx(p, me, kPhCout, 0, false, false), -1);
   }
-  if (L > 0 && !p.loopback) dbarrier(p, me, 2 * L, barrier_npeers(t, 2 * L), e, group_peer(2 * L));
+  if (L > 0 && !p.loopback) {
+    if (!(p.mode & kCoutAll) && !settle(last_phase + 1)) return;
+    if (!dbarrier(p, me, 2 * L, barrier_npeers(t, 2 * L), e, group_peer(2 * L))) return;
+  }
   trace_ev(p, me, 2 + 2 * (2 * L));
+  rank_epoch_end(p, me, e, STEAL ? 2 * L : 0);
 }
 
 // ------------------------------------------------------------------------ rank-level, dynamic (PATH 3)
@@ -712,26 +1064,6 @@ __global__ void __launch_bounds__(kThreads, PATH == 2 ? DDL_TMA_MINBLOCKS : 1) d
 // Rank state (in each rank's flag region, after the per-CTA area):
 //   [0] call epoch of this rank, then arrive[j] / work[j] counters per phase j (pre-phase =
 //   kPrePhase), then flags[slot][src]: src signalled slot with its epoch.
-constexpr int kNumSlots = 2 * kMaxDims + 1;
-constexpr int kPrePhase = kNumSlots;      // copy-in / nothing, before barrier 0
-constexpr int kPostPhase = kNumSlots + 1; // copy-out, after the end barrier
-constexpr int kRankStateWords = 16 + 2 * (kNumSlots + 2) + kNumSlots * kMaxRanks;
-
-__device__ __forceinline__ uint32_t* rank_state(const KParams& p, int r) {
-  return p.flags[r] + p.cmax + (size_t)kNumSlots * p.cmax * p.t.P;
-}
-__device__ __forceinline__ uint32_t* rs_arrive(uint32_t* rs, int j) { return rs + 16 + j; }
-__device__ __forceinline__ uint32_t* rs_work(uint32_t* rs, int j) { return rs + 16 + (kNumSlots + 2) + j; }
-__device__ __forceinline__ uint32_t* rs_flag(uint32_t* rs, int slot, int src) {
-  return rs + 16 + 2 * (kNumSlots + 2) + slot * kMaxRanks + src;
-}
-
-__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* a, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
-  return old;
-}
-
 // Barrier-slot peer lists: barrier j's group (j < 2L) or every group (j = 2L), plus r itself
 // (its own other CTAs wrote data this rank reads next).  Lane l < npeers+1.
 __device__ __forceinline__ int rank_barrier_member(const Topo& t, int me, int slot, int l) {
@@ -926,10 +1258,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_dyn_kernel(const __grid_constant__ KParams p) {
   const int me = p.loopback ? (int)blockIdx.y : p.rank;
   uint32_t* rs = rank_state(p, me);
-  __shared__ uint32_t s_e;
-  if (threadIdx.x == 0) s_e = *rs + 1;  // this rank's call number (CTA 0 stores it at the end)
-  __syncthreads();
-  const uint32_t e = s_e;
+  const uint32_t e = rank_epoch_begin(p, me);
   if (me == p.skip_rank) return;
   const Topo& t = p.t;
   const int L = t.nlive;
@@ -960,8 +1289,8 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_dyn_kernel(co
     dyn_phase<T>(p, me, phase_ctx(p, me, kPhCout, 0, false, false), pp, rs_work(rs, kPostPhase));
     rank_arrive(p, me, kPostPhase, -1, e);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *rs = e;
   trace_ev(p, me, 2 + 2 * (2 * L));
+  rank_epoch_end(p, me, e, 0);
 }
 
 // ------------------------------------------------------------------------ one-shot (a9)
@@ -995,13 +1324,13 @@ __device__ __forceinline__ void nested_feed(const KParams& p, const int* gl, con
   }
 }
 
-template <typename T, int K>
+template <typename T, int K, int R>
 __global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_constant__ KParams p) {
   using A = typename Tr<T>::Acc;
   constexpr int W = Tr<T>::W;
   constexpr int CH = 8;
   const int me = p.loopback ? (int)blockIdx.y : p.rank;
-  const uint32_t e = next_epoch(p, me);
+  const uint32_t e = rank_epoch_begin(p, me);
   if (me == p.skip_rank) return;
   const Topo& t = p.t;
   const int P = t.P;
@@ -1011,58 +1340,70 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_c
     gl[j] = t.g[t.live[j]];
     Gl[j] = t.G[t.live[j]];
   }
+  // R vectors per thread, strided by the CTA width: item i covers elements eoff[i] .. +W
   const uint64_t lo = (uint64_t)blockIdx.x * p.slice;
-  const uint64_t eoff = lo + (uint64_t)threadIdx.x * W;   // one vector per thread
   const uint64_t hi = lo + p.slice < p.n ? lo + p.slice : p.n;
-  const bool full = eoff + W <= hi;
-  const int ntail = (!full && eoff < hi) ? (int)(hi - eoff) : 0;
   auto all = [me](int l) { return all_peer(me, l); };
 
   if (p.mode & kCinAll) {  // staged: publish this CTA's slice of my input
     const char* s = static_cast<const char*>(p.cin[me]);
     char* w = static_cast<char*>(p.work[me]);
-    if (full) st_vec(w + eoff * sizeof(T), ld_vec(s + eoff * sizeof(T)));
-    for (int i = 0; i < ntail; ++i)
-      st_elem<T>(w + (eoff + i) * sizeof(T), ld_elem<T>(s + (eoff + i) * sizeof(T)));
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint64_t eo = lo + ((uint64_t)i * blockDim.x + threadIdx.x) * W;
+      if (eo + W <= hi) st_vec(w + eo * sizeof(T), ld_vec(s + eo * sizeof(T)));
+      else
+        for (uint64_t x = eo; x < hi; ++x) st_elem<T>(w + x * sizeof(T), ld_elem<T>(s + x * sizeof(T)));
+    }
   }
   // loopback without copy-in: inputs are ready at launch (see ddl_hier_kernel)
   if (!(p.loopback && !(p.mode & kCinAll)) && !dbarrier(p, me, 0, P - 1, e, all)) return;
 
-  A res[W];
-  if (full) {
-    A lvl[K][W];
-    for (int r0 = 0; r0 < P; r0 += CH) {
-      uint4 raw[CH];
+  A res[R][W];
 #pragma unroll
-      for (int i = 0; i < CH; ++i) {
-        if (r0 + i >= P) break;
-        raw[i] = ld_vec(static_cast<const char*>(p.in[r0 + i]) + eoff * sizeof(T));
-      }
+  for (int i = 0; i < R; ++i) {
+    const uint64_t eoff = lo + ((uint64_t)i * blockDim.x + threadIdx.x) * W;
+    const bool full = eoff + W <= hi;
+    const int ntail = (!full && eoff < hi) ? (int)(hi - eoff) : 0;
+    if (full) {
+      A lvl[K][W];
+      for (int r0 = 0; r0 < P; r0 += CH) {
+        uint4 raw[CH];
 #pragma unroll
-      for (int i = 0; i < CH; ++i) {
-        if (r0 + i >= P) break;
-        A x[W];
-        unpack<T>(raw[i], x);
-        nested_feed<T, K, W>(p, gl, Gl, r0 + i, lvl, x, res);
+        for (int k = 0; k < CH; ++k) {
+          if (r0 + k >= P) break;
+          raw[k] = ld_vec(static_cast<const char*>(p.in[r0 + k]) + eoff * sizeof(T));
+        }
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          if (r0 + k >= P) break;
+          A x[W];
+          unpack<T>(raw[k], x);
+          nested_feed<T, K, W>(p, gl, Gl, r0 + k, lvl, x, res[i]);
+        }
       }
-    }
-  } else {
-    for (int k = 0; k < ntail; ++k) {  // ragged end of the vector, one element at a time
-      A lvl1[K][1];
-      A r1[1];
-      for (int r = 0; r < P; ++r) {
-        A x[1] = {Tr<T>::to(ld_elem<T>(static_cast<const char*>(p.in[r]) + (eoff + k) * sizeof(T)))};
-        nested_feed<T, K, 1>(p, gl, Gl, r, lvl1, x, r1);
+    } else {
+      for (int k = 0; k < ntail; ++k) {  // ragged end of the vector, one element at a time
+        A lvl1[K][1];
+        A r1[1];
+        for (int r = 0; r < P; ++r) {
+          A x[1] = {Tr<T>::to(ld_elem<T>(static_cast<const char*>(p.in[r]) + (eoff + k) * sizeof(T)))};
+          nested_feed<T, K, 1>(p, gl, Gl, r, lvl1, x, r1);
+        }
+        res[i][k] = r1[0];
       }
-      res[k] = r1[0];
     }
   }
   if (!dbarrier(p, me, 1, P - 1, e, all)) return;
   char* o = static_cast<char*>(p.out[me]);
-  if (full) st_vec(o + eoff * sizeof(T), pack<T>(res));
-  for (int k = 0; k < ntail; ++k) st_elem<T>(o + (eoff + k) * sizeof(T), Tr<T>::from(res[k]));
-  if (p.mode & kCoutAll) {  // (unused: the staged one-shot writes the user buffer directly)
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const uint64_t eoff = lo + ((uint64_t)i * blockDim.x + threadIdx.x) * W;
+    if (eoff + W <= hi) st_vec(o + eoff * sizeof(T), pack<T>(res[i]));
+    else
+      for (uint64_t x = eoff; x < hi; ++x) st_elem<T>(o + x * sizeof(T), Tr<T>::from(res[i][x - eoff]));
   }
+  rank_epoch_end(p, me, e, 0);
 }
 
 // ------------------------------------------------------------------------ K5 local reduce

@@ -85,12 +85,13 @@ struct ddl_comm {
   size_t lb_ws_bytes = 0;  // per virtual rank
   int* err = nullptr;      // sticky device error
   ddl_algo_t algo = DDL_ALGO_AUTO;
-  size_t oneshot_max = 256 << 10;
+  size_t oneshot_max = 512 << 10;  // crossover measured in loopback (profiles/r01_oneshot_crossover.txt)
   size_t min_slice_bytes = 16 << 10;
   int ctas_limit = 0;  // 0 = occupancy bound
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int skip_rank = -1;
   bool use_tma = true;
+  bool use_steal = false;  // DDL_STEAL=1: per-CTA slices + work stealing (PATH 4)
   bool use_dyn = false;  // DDL_DYN=1: rank-level barriers + dynamic chunks (measured slower)
   int gpu_share = 1;
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)  // ranks sharing this GPU (loopback: P; in-process test groups: P)
@@ -128,6 +129,7 @@ void apply_env(ddl_comm* c) {
   c->ctas_limit = (int)env_size("DDL_CTAS", 0);
   c->use_tma = env_size("DDL_NO_TMA", 0) == 0;
   c->use_dyn = env_size("DDL_DYN", 0) != 0;
+  c->use_steal = env_size("DDL_STEAL", 0) != 0;
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
@@ -147,7 +149,8 @@ ddl_result_t common_init(ddl_comm* c, int nranks, const int* dims, int ndims, in
   DDL_CUDA(cudaSetDevice(dev));
   DDL_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
   c->cmax = c->num_sms * 4;
-  const size_t words = (size_t)c->cmax * (1 + (size_t)kNumSlots * nranks) + kRankStateWords;
+  const size_t words = (size_t)c->cmax * (1 + (size_t)kNumSlots * nranks) + kRankStateWords +
+                       16 + 2 * (size_t)kNumSlots * c->cmax;  // + steal counters
   c->flags_bytes = (words * 4 + 65535) / 65536 * 65536;
   apply_env(c);
   if (env_size("DDL_TRACE", 0)) {
@@ -167,23 +170,29 @@ struct Plan {
   int path = 2;  // hierarchical kernel variant: 0 element-wise, 1 register-staged, 2 TMA-staged,
                  // 3 TMA-staged with rank-level barriers and dynamic chunks
   bool oneshot = false;
+  int r = 1;  // one-shot: vectors per thread
 };
 
 template <typename T>
 const void* hier_fn(int path) {
+  if (path == 4) return (const void*)ddl_hier_kernel<T, 4>;
   if (path == 3) return (const void*)ddl_dyn_kernel<T>;
   if (path == 2) return (const void*)ddl_hier_kernel<T, 2>;
   return path == 1 ? (const void*)ddl_hier_kernel<T, 1> : (const void*)ddl_hier_kernel<T, 0>;
 }
-template <typename T>
-const void* oneshot_fn(int K) {
+template <typename T, int R>
+const void* oneshot_fn_r(int K) {
   switch (K) {
-    case 1: return (const void*)ddl_oneshot_kernel<T, 1>;
-    case 2: return (const void*)ddl_oneshot_kernel<T, 2>;
-    case 3: return (const void*)ddl_oneshot_kernel<T, 3>;
-    case 4: return (const void*)ddl_oneshot_kernel<T, 4>;
+    case 1: return (const void*)ddl_oneshot_kernel<T, 1, R>;
+    case 2: return (const void*)ddl_oneshot_kernel<T, 2, R>;
+    case 3: return (const void*)ddl_oneshot_kernel<T, 3, R>;
+    case 4: return (const void*)ddl_oneshot_kernel<T, 4, R>;
     default: return nullptr;
   }
+}
+template <typename T>
+const void* oneshot_fn(int K, int R) {
+  return R == 4 ? oneshot_fn_r<T, 4>(K) : R == 2 ? oneshot_fn_r<T, 2>(K) : oneshot_fn_r<T, 1>(K);
 }
 const void* hier_fn_dt(ddl_dtype_t dt, int path) {
   if (dt == DDL_INT32) return hier_fn<int32_t>(path);
@@ -191,10 +200,10 @@ const void* hier_fn_dt(ddl_dtype_t dt, int path) {
   return hier_fn<__nv_bfloat16>(path);
 }
 size_t hier_smem(int path) { return path >= 2 ? kTmaSmem : 0; }
-const void* oneshot_fn_dt(ddl_dtype_t dt, int K) {
-  if (dt == DDL_INT32) return oneshot_fn<int32_t>(K);
-  if (dt == DDL_FLOAT32) return oneshot_fn<float>(K);
-  return oneshot_fn<__nv_bfloat16>(K);
+const void* oneshot_fn_dt(ddl_dtype_t dt, int K, int R) {
+  if (dt == DDL_INT32) return oneshot_fn<int32_t>(K, R);
+  if (dt == DDL_FLOAT32) return oneshot_fn<float>(K, R);
+  return oneshot_fn<__nv_bfloat16>(K, R);
 }
 
 // CTAs per rank that may be resident at once (loopback: all P ranks share the GPU).
@@ -212,7 +221,7 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
   pl.vec = vec;
   const int w = elem_size(dt);
   const uint64_t W = vec ? 16 / w : 1;
-  pl.path = !vec ? 0 : (c->use_tma ? (c->use_dyn ? 3 : 2) : 1);
+  pl.path = !vec ? 0 : (c->use_tma ? (c->use_dyn ? 3 : (c->use_steal ? 4 : 2)) : 1);
   int cap = cap_per_rank(c, hier_fn_dt(dt, pl.path), hier_smem(pl.path));
   if (pl.path >= 2 && q * w < c->tma_min_slice_bytes * (uint64_t)cap) {
     // small per-CTA slices: the register-staged path has lower per-phase latency
@@ -234,17 +243,21 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
 
 bool plan_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
   const int K = c->topo.nlive;
-  const void* fn = oneshot_fn_dt(dt, K);
-  if (!fn) return false;
-  const uint64_t per_cta = (uint64_t)kThreads * (16 / elem_size(dt));
-  const uint64_t ctas = (n + per_cta - 1) / per_cta;
-  if (ctas > (uint64_t)cap_per_rank(c, fn)) return false;
-  pl->oneshot = true;
-  pl->vec = true;
-  pl->q = 0;
-  pl->slice = per_cta;
-  pl->nctas = (int)ctas;
-  return true;
+  for (int R : {1, 2, 4}) {  // fewest vectors per thread that fit the resident CTAs
+    const void* fn = oneshot_fn_dt(dt, K, R);
+    if (!fn) return false;
+    const uint64_t per_cta = (uint64_t)kThreads * R * (16 / elem_size(dt));
+    const uint64_t ctas = (n + per_cta - 1) / per_cta;
+    if (ctas > (uint64_t)cap_per_rank(c, fn)) continue;
+    pl->oneshot = true;
+    pl->vec = true;
+    pl->q = 0;
+    pl->r = R;
+    pl->slice = per_cta;
+    pl->nctas = (int)ctas;
+    return true;
+  }
+  return false;
 }
 
 bool use_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
@@ -272,7 +285,7 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
 }
 
 ddl_result_t launch(const ddl_comm* c, const KParams& p, const Plan& pl, ddl_dtype_t dt, void* stream) {
-  const void* fn = pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive) : hier_fn_dt(dt, pl.path);
+  const void* fn = pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive, pl.r) : hier_fn_dt(dt, pl.path);
   if (!fn) return DDL_ERR_UNSUPPORTED;
   const size_t smem = pl.oneshot ? 0 : hier_smem(pl.path);
   blocks_per_sm(fn, smem);  // sets the dynamic shared-memory attribute once

@@ -101,7 +101,7 @@ def test_auto_algo_switch_is_invisible():
                 lb.set_algo(algo, 1 << 40)
                 outs.append(run_allreduce(lb, bufs, dtype, "avg"))
             assert all(same_bits(a, b) for a, b in zip(*outs))
-    lb.set_algo(ddl.ALGO_AUTO, 256 << 10)
+    lb.set_algo(ddl.ALGO_AUTO, 512 << 10)
 
 
 def test_repeated_calls_varying_sizes():
@@ -201,7 +201,7 @@ def test_config2_resnet50_buckets_8x_2x4():
     8 ranks, dims 2x4 = [4, 2]."""
     P, dims = 8, ddl.parse_dims("2x4")
     lb = loopback(P, dims)
-    lb.set_algo(ddl.ALGO_AUTO, 256 << 10)
+    lb.set_algo(ddl.ALGO_AUTO, 512 << 10)
     for b in range(len(si.resnet50_bucket_bytes())):
         bufs = [si.resnet50_bucket(b, r) for r in range(P)]
         dev = [to_dev(x, "float32") for x in bufs]
@@ -252,3 +252,44 @@ def test_int32_bitmask_256MiB_closed_form():
     want = ((((1 << P) - 1) + P * ((i % (1 << 20)) << 8)) & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
     for t in dev:
         assert np.array_equal(to_host(t), want)
+
+
+# ------------------------------------------------------------------ alternative kernel paths
+PATH_ENVS = {"steal": "DDL_STEAL", "dyn": "DDL_DYN", "ldg": "DDL_NO_TMA", "tma-all": "DDL_TMA_MIN_SLICE_BYTES"}
+
+
+@pytest.mark.parametrize("path", sorted(PATH_ENVS))
+@pytest.mark.parametrize("P,dims", [(8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (6, [3, 2]), (4, [2, 2])])
+def test_kernel_paths_parity(path, P, dims):
+    """Every hierarchical kernel variant (register-staged, TMA-staged for all sizes, work
+    stealing, rank-level dynamic) computes the same bits as the oracle."""
+    import os
+    var = PATH_ENVS[path]
+    old = os.environ.get(var)
+    os.environ[var] = "0" if var == "DDL_TMA_MIN_SLICE_BYTES" else "1"
+    try:
+        lb = ddl.Loopback(P, dims)
+    finally:
+        if old is None:
+            os.environ.pop(var, None)
+        else:
+            os.environ[var] = old
+    lb.set_algo(ddl.ALGO_HIER, 0)
+    for dtype in ("int32", "float32", "bfloat16"):
+        for n in (1, 7, 40_003, 1_000_003, 3_000_017):
+            op = "sum" if dtype == "int32" else "avg"
+            bufs = si.rank_buffers(dtype, KIND[dtype], n, P, seed=n)
+            want = oracle.allreduce(bufs, dims, dtype, op)
+            got = run_allreduce(lb, bufs, dtype, op)
+            for r in range(P):
+                assert same_bits(got[r], want[r]), (path, dims, dtype, n, r, first_diff(got[r], want[r]))
+    # reduce-scatter / allgather through the same variant
+    recv = 65_536 + 8
+    bufs = si.rank_buffers("float32", "normal", P * recv, P, seed=3)
+    want = oracle.reduce_scatter(bufs, dims, "float32", "sum")
+    sends = [to_dev(b, "float32") for b in bufs]
+    outs = [torch.empty(recv, device="cuda") for _ in range(P)]
+    lb.reduce_scatter(outs, sends)
+    torch.cuda.synchronize()
+    assert all(same_bits(to_host(outs[r]), want[r]) for r in range(P))
+    lb.finalize()
