@@ -45,6 +45,17 @@ NVLINK_MEASURED_PEER = 770.0   # B200_PROFILING.md: measured peer copy per direc
 DIMS_FOR_N = {1: "2x4", 2: "2", 4: "2x2", 8: "2x4"}
 
 
+def profiled_traffic(workload_key: str):
+    """DRAM bytes per step of the timed kernels from the committed ncu capture
+    (profiles/traffic.json, written from an `ncu --set full` run of scripts/profile_step.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d["dram_bytes_per_step"] if d.get("workload") == workload_key else None
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -238,6 +249,8 @@ def run_loopback(args):
     ms = t_start.elapsed_time(t_end) / args.steps
     busbw = S_total * 2 * (P - 1) / P / (ms * 1e-3) / 1e9
     kern_ms = sum(evs[k][b][0].elapsed_time(evs[k][b][1]) for k in range(args.steps) for b in range(nb))
+    bucket_us = [sum(evs[k][b][0].elapsed_time(evs[k][b][1]) for k in range(args.steps)) / args.steps * 1e3
+                 for b in range(nb)]
     algo_bytes = sum(loopback_hbm_bytes(n, P, dims, 4) for n in sizes) * args.steps
     hbm_peak, peak_src = peaks()
     achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
@@ -291,9 +304,13 @@ def run_loopback(args):
                    "dims": "x".join(map(str, dims[::-1])), "n_ranks": P, "bytes_per_rank": S_total,
                    "buckets": sizes, "l2": "inputs (8 x 102 MB) larger than L2, no flush",
                    "algo": ["oneshot" if lb.algo_for(s, "float32") == ddl.ALGO_ONESHOT else "hier" for s in sizes],
-                   "ctas_per_rank": [lb.ctas_for(s, "float32") for s in sizes]},
+                   "ctas_per_rank": [lb.ctas_for(s, "float32") for s in sizes],
+                   "bucket_us": [round(u, 1) for u in bucket_us]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak,
+                     "traffic": profiled_traffic("resnet50-grad-set 8 virtual ranks dims 2x4 avg")
+                     if dims == [4, 2] else None,
+                     "traffic_unit": "DRAM bytes per step (all 5 launches), ncu --set full, profiles/traffic.json",
                      "peak_source": peak_src,
                      "kernel": "ddl_hier_kernel<float,true> (loopback, all 8 virtual ranks)",
                      "algorithmic_bytes_per_step": algo_bytes // args.steps,

@@ -267,7 +267,7 @@ class Comm:
                                   DTYPE_CODES[dtype_name(out)], _stream(stream)), "ddl_allgather")
         return out
 
-    def set_algo(self, algo: int, oneshot_max_bytes: int = 256 << 10) -> None:
+    def set_algo(self, algo: int, oneshot_max_bytes: int = 512 << 10) -> None:
         _check(_lib.ddl_set_algo(self.h, algo, oneshot_max_bytes), "ddl_set_algo")
 
     def async_error(self) -> int:
@@ -336,7 +336,7 @@ class Loopback:
                "ddl_group_allgather")
         return outs
 
-    def set_algo(self, algo: int, oneshot_max_bytes: int = 256 << 10) -> None:
+    def set_algo(self, algo: int, oneshot_max_bytes: int = 512 << 10) -> None:
         _check(_lib.ddl_set_algo(self.h, algo, oneshot_max_bytes), "ddl_set_algo")
 
     def set_timeout(self, ms: int) -> None:
@@ -435,7 +435,7 @@ class InProcessGroup:
                                                           inps[r].numel(), dt, s), "ddl_allgather"))
         return outs
 
-    def set_algo(self, algo: int, oneshot_max_bytes: int = 256 << 10) -> None:
+    def set_algo(self, algo: int, oneshot_max_bytes: int = 512 << 10) -> None:
         for h in self.hs:
             _check(_lib.ddl_set_algo(h, algo, oneshot_max_bytes), "ddl_set_algo")
 
