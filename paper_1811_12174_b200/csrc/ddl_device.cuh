@@ -63,6 +63,7 @@ struct KParams {
   void* cout[kMaxRanks];        // copy-out destination of each rank
   int mode;
   uint64_t* trace;     // debug (DDL_TRACE=1): [P][cmax][kTraceEvents] globaltimer stamps, else null
+  int stream_every;    // PATH 5: publish progress every k chunks (and at the phase end)
 };
 constexpr int kTraceEvents = 40;
 
@@ -560,7 +561,7 @@ __device__ void ldg_phase(const KParams& p, int me, const PhaseCtx& x) {
 #endif
 constexpr int kStages = DDL_TMA_STAGES;
 constexpr uint32_t kStageBytes = DDL_TMA_STAGE_KB * 1024;
-constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t);
+constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t) + 16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
   return (uint32_t)__cvta_generic_to_shared(ptr);
@@ -595,16 +596,21 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 struct Pipe {
   char* smem;
   uint64_t* bar;
-  uint32_t seq;  // chunks consumed so far by this CTA (identical in every thread)
+  uint32_t* stored;  // PATH 5: consumer warps that finished storing a chunk (monotone, smem)
+  uint32_t seq;      // chunks consumed so far by this CTA (identical in every thread)
+  uint32_t sseq;     // chunks counted in *stored so far (stream phases only)
 };
 
 __device__ __forceinline__ void pipe_init(Pipe& pp) {
   extern __shared__ __align__(128) char dsmem[];
   pp.smem = dsmem;
   pp.bar = reinterpret_cast<uint64_t*>(dsmem + (size_t)kStages * kStageBytes);
+  pp.stored = reinterpret_cast<uint32_t*>(pp.bar + kStages);
   pp.seq = 0;
+  pp.sseq = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&pp.bar[s], 1);
+    *pp.stored = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -964,6 +970,251 @@ __device__ void steal_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& p
   if (threadIdx.x == 0 && cnt) red_release_add(&done[cnt_slice], cnt);
 }
 
+// ------------------------------------------------------------------------ streaming (PATH 5)
+// PATH 2 without the inner phase barriers: every CTA publishes, per data phase, how many of
+// its chunks are done (a 64-bit (epoch << 32 | count) word, st.release after each chunk), and
+// the producer thread of a consumer CTA waits, per chunk it is about to load, only for the
+// producer chunks that cover exactly the bytes it needs.  With static slices the producer of
+// slice c of any block is always CTA c of the source rank, so the dependency is a count, not
+// a barrier: phase d+1 of a slice starts as soon as its first source chunks exist, while
+// slower CTAs are still finishing phase d.  (Start and end barriers stay.)
+__device__ __forceinline__ uint64_t* prog_word(const KParams& p, int r, int jphase) {
+  uint32_t* end = steal_base(p, r) + 16 + 2 * (size_t)kNumSlots * p.cmax;
+  uint64_t* base = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(end) + 7) & ~(uintptr_t)7);
+  return base + (size_t)jphase * p.cmax;
+}
+__device__ __forceinline__ void st_release64(uint64_t* a, uint64_t v, bool gpu_scope) {
+  if (gpu_scope) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+  else asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire64(const uint64_t* a, bool gpu_scope) {
+  uint64_t v;
+  if (gpu_scope) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  else asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ PhaseCtx data_phase(const KParams& p, int m, int jj) {
+  const int L = p.t.nlive;
+  if (jj < L) return phase_ctx(p, m, kPhRS, p.t.live[jj], jj == 0, jj == L - 1);
+  return phase_ctx(p, m, kPhAG, p.t.live[2 * L - 1 - jj], false, false);
+}
+__device__ __forceinline__ uint32_t phase_cb(const PhaseCtx& x) { return (kStageBytes / (uint32_t)x.g) & ~15u; }
+
+// The data phase in which rank m last wrote block b (-1: before the first barrier).
+__device__ __forceinline__ int final_phase(const KParams& p, int b, int m) {
+  const Topo& t = p.t;
+  const int L = t.nlive;
+  if (b == m) return (p.mode & kRS) ? L - 1 : -1;
+  int idx = -1;
+  for (int i = 0; i < L; ++i)
+    if (coord(t, b, t.live[i]) != coord(t, m, t.live[i])) idx = i;
+  return 2 * L - 1 - idx;  // AG phase of the outermost dim where b and m differ
+}
+
+// Where block b (slice c) sits in rank m's phase jj: chunks before its unit, its own chunk
+// count, the phase's total, and the phase's chunk bytes.
+template <typename T>
+__device__ void locate(const KParams& p, int m, int jj, int b, int c, uint32_t* before, uint32_t* own,
+                       uint32_t* total, uint32_t* cb) {
+  constexpr int W = Tr<T>::W;
+  const PhaseCtx x = data_phase(p, m, jj);
+  const uint32_t CB = phase_cb(x);
+  uint32_t acc = 0, mine = 0, pre = 0;
+  for (int u = 0; u < x.nunits; ++u) {
+    int sr;
+    const int bu = unit_block(p, m, x, u, &sr);
+    uint64_t e0;
+    uint32_t vb, rem;
+    slice_unit_span<W, T>(p, bu, c, &e0, &vb, &rem);
+    const uint32_t k = (vb + CB - 1) / CB;
+    if (bu == b) {
+      pre = acc;
+      mine = k;
+    }
+    acc += k;
+  }
+  *before = pre;
+  *own = mine;
+  *total = acc;
+  *cb = CB;
+}
+
+template <typename T>
+__device__ void stream_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp, int jphase, bool wait,
+                             uint32_t epoch) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = Tr<T>::W;
+  __shared__ UnitDesc s_units[kMaxRanks];
+  __shared__ const char* s_srcs[kMaxRanks];
+  // per (unit, source): source rank, its phase, chunks before the block there, chunk bytes,
+  // the block's chunks, the phase total
+  __shared__ int s_nr[kMaxRanks][kMaxRanks], s_np[kMaxRanks][kMaxRanks];
+  __shared__ uint32_t s_nb[kMaxRanks][kMaxRanks], s_ncb[kMaxRanks][kMaxRanks], s_nown[kMaxRanks][kMaxRanks],
+      s_ntot[kMaxRanks][kMaxRanks];
+  const uint32_t CB = phase_cb(x);
+  const bool rs = x.kind == kPhRS;
+  const bool do_scale = rs && x.last && p.op == kAvg;
+  const int c = blockIdx.x;
+  const int nsrc = rs ? x.g : 1;
+  char* dst = dst_base(p, me, x);
+  fill_units<T, W>(p, me, x, s_units, s_srcs, nullptr);
+  uint32_t total = 0;
+  for (int u = 0; u < x.nunits; ++u) total += (s_units[u].bytes + CB - 1) / CB;
+  const uint64_t ehi = (uint64_t)epoch << 32;
+  uint64_t* myprog = prog_word(p, me, jphase) + c;
+
+  if (wait && threadIdx.x == 0) {  // dependency tables
+    for (int u = 0; u < x.nunits; ++u) {
+      int sr;
+      const int b = unit_block(p, me, x, u, &sr);
+      for (int v = 0; v < nsrc; ++v) {
+        const int m = rs ? member(p.t, me, x.d, v) : sr;
+        const int ph = rs ? jphase - 1 : final_phase(p, b, m);
+        s_nr[u][v] = m;
+        s_np[u][v] = (m == me || ph < 0) ? -1 : ph;  // own data: written by this CTA already
+        if (s_np[u][v] >= 0) locate<T>(p, m, ph, b, c, &s_nb[u][v], &s_nown[u][v], &s_ntot[u][v], &s_ncb[u][v]);
+      }
+    }
+  }
+  auto wait_for = [&](int u, uint32_t end_bytes, bool whole_phase) -> bool {
+    for (int v = 0; v < nsrc; ++v) {
+      const int ph = s_np[u][v];
+      if (ph < 0) continue;
+      uint32_t need = whole_phase ? s_ntot[u][v] + 1
+                                  : s_nb[u][v] + min(s_nown[u][v], (end_bytes + s_ncb[u][v] - 1) / s_ncb[u][v]);
+      const uint64_t* w = prog_word(p, s_nr[u][v], ph) + c;
+      uint64_t t0 = 0;
+      uint32_t spins = 0;
+      while (ld_acquire64(w, p.loopback) < (ehi | need)) {
+        if ((++spins & 1023u) == 0) {
+          const uint64_t now = globaltimer();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > p.timeout_ns) {
+            atomicExch(p.err, kErrTimeout);
+            return false;
+          }
+        }
+      }
+    }
+    return true;
+  };
+
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) s_fail = 0;
+  int pu = 0;
+  uint32_t poff = 0;
+  bool failed = false;
+  auto issue = [&](uint32_t sq) {
+    while (poff >= s_units[pu].bytes) {
+      ++pu;
+      poff = 0;
+    }
+    const UnitDesc ud = s_units[pu];
+    const uint32_t bytes = min(CB, ud.bytes - poff);
+    const int st = (int)(sq % kStages);
+    char* sbase = pp.smem + (size_t)st * kStageBytes;
+    const size_t go = ud.e0 * sizeof(T) + poff;
+    if (wait && !failed) {
+      if (!wait_for(pu, poff + bytes, false)) failed = true;
+      fence_proxy_async_global();
+    }
+    mbar_arm(&pp.bar[st], failed ? 0 : bytes * (uint32_t)x.g);
+    if (!failed) {
+      if (rs) {
+        for (int v = 0; v < x.g; ++v) tma_load(sbase + (size_t)v * CB, s_srcs[v] + go, bytes, &pp.bar[st]);
+      } else {
+        tma_load(sbase, ud.src + go, bytes, &pp.bar[st]);
+      }
+    }
+    poff += bytes;
+  };
+  if (threadIdx.x == 0 && total) {
+    fence_proxy_async_global();
+    for (uint32_t j = 0; j < total && j < (uint32_t)kStages; ++j) issue(pp.seq + j);
+  }
+
+  // warps 0..14 consume; warp 15 only publishes progress (its release fences never stall
+  // the consumers): each consumer warp counts itself in *pp.stored after storing a chunk
+  // (release, CTA scope); the signal lane waits for all 15 and releases (epoch << 32 | chunks
+  // done) at GPU/system scope -- cumulative over the warps' stores.
+  constexpr uint32_t kCons = kThreads - 32;
+  const bool signaller = threadIdx.x >= kCons;
+  if (signaller) {
+    if (threadIdx.x == kCons) {
+      for (uint32_t j = 0; j < total; ++j) {
+        const uint32_t want = (pp.sseq + j + 1) * (kCons / 32);  // every consumer warp stored chunk j
+        uint32_t got;
+        do {
+          asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(got) : "r"(smem_u32(pp.stored)) : "memory");
+        } while ((int32_t)(got - want) < 0);
+        if ((j + 1) % p.stream_every == 0 || j + 1 == total) st_release64(myprog, ehi | (j + 1), p.loopback);
+      }
+    }
+  }
+  int cu = 0;
+  uint32_t coff = 0;
+  for (uint32_t j = 0; j < total && !signaller; ++j) {
+    while (coff >= s_units[cu].bytes) {
+      ++cu;
+      coff = 0;
+    }
+    const uint32_t bytes = min(CB, s_units[cu].bytes - coff);
+    const uint32_t sq = pp.seq + j;
+    const int st = (int)(sq % kStages);
+    const char* sbase = pp.smem + (size_t)st * kStageBytes;
+    char* pd = dst + s_units[cu].e0 * sizeof(T) + coff;
+    mbar_wait(&pp.bar[st], (sq / kStages) & 1u);
+    const uint32_t nv = bytes / 16u;
+    if (rs) {
+      for (uint32_t i = threadIdx.x; i < nv; i += kCons) {
+        A acc[W];
+        unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)i * 16), acc);
+        for (int v = 1; v < x.g; ++v) {
+          A y[W];
+          unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)v * CB + (size_t)i * 16), y);
+#pragma unroll
+          for (int k = 0; k < W; ++k) acc[k] = Tr<T>::add(acc[k], y[k]);
+        }
+        if (do_scale) {
+#pragma unroll
+          for (int k = 0; k < W; ++k) acc[k] = Tr<T>::mul(acc[k], p.scale);
+        }
+        st_vec(pd + (size_t)i * 16, pack<T>(acc));
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < nv; i += kCons)
+        st_vec(pd + (size_t)i * 16, *reinterpret_cast<const uint4*>(sbase + (size_t)i * 16));
+    }
+    coff += bytes;
+    __syncwarp();  // this warp's stores of the chunk precede lane 0's release below
+    if ((threadIdx.x & 31) == 0)
+      asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(pp.stored)) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(kCons) : "memory");  // stage st consumed by all consumers
+    if (threadIdx.x == 0 && j + kStages < total) issue(sq + kStages);
+  }
+  __syncthreads();  // the signal warp has published every chunk
+  pp.seq += total;
+  pp.sseq += total;
+  if (threadIdx.x == 0 && failed) s_fail = 1;
+  // ragged remainders: their sources must have finished the whole producing phase
+  bool any_rem = false;
+  for (int u = 0; u < x.nunits; ++u) any_rem |= s_units[u].rem != 0;
+  if (any_rem) {
+    if (wait && threadIdx.x == 0 && !failed) {
+      for (int u = 0; u < x.nunits; ++u)
+        if (s_units[u].rem && !wait_for(u, 0, true)) {
+          s_fail = 1;
+          break;
+        }
+    }
+    __syncthreads();
+    ragged_tails<T>(p, x, dst, s_units, s_srcs);
+  }
+  __syncthreads();
+  if (threadIdx.x == 32) st_release64(myprog, ehi | (total + 1), p.loopback);  // phase complete
+}
+
 // ------------------------------------------------------------------------ the hierarchical kernel
 // PATH: 0 = element-wise loads (unaligned RS/AG layouts), 1 = 16-byte register-staged
 // loads, 2 = 16-byte TMA-staged (default), 4 = TMA-staged with work stealing.
@@ -972,6 +1223,7 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
   constexpr bool VEC = PATH >= 1;
   constexpr bool TMA = PATH >= 2;
   constexpr bool STEAL = PATH == 4;
+  constexpr bool STREAM = PATH == 5;
   const int me = p.loopback ? (int)blockIdx.y : p.rank;
   const uint32_t e = rank_epoch_begin(p, me);
   if (me == p.skip_rank) return;
@@ -983,6 +1235,13 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
   if constexpr (TMA) pipe_init(pp);
 
   auto run = [&](const PhaseCtx& x, int j) {
+    if constexpr (STREAM) {
+      if (x.kind == kPhRS || x.kind == kPhAG) {
+        const int first = (p.mode & kRS) ? 0 : L;
+        stream_phase<T>(p, me, x, pp, j, j > first, e);
+        return;
+      }
+    }
     if constexpr (STEAL) {
       if (x.kind == kPhRS || x.kind == kPhAG) {
         steal_phase<T>(p, me, x, pp, j);
@@ -1015,7 +1274,9 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
   if (p.mode & kRS) {
     for (int j = 0; j < L; ++j) {
       if (!settle(j)) return;
-      if (!(j == 0 && implied_start) && !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
+      if (!(j == 0 && implied_start) && !(STREAM && j > 0) &&
+          !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j)))
+        return;
       trace_ev(p, me, 2 + 2 * j);
       prev = phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1);
       run(prev, j);
@@ -1027,7 +1288,8 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
     for (int jj = 0; jj < L; ++jj) {
       const int j = L + jj;
       if (!settle(j)) return;
-      if (!dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j))) return;
+      if (!(STREAM && (jj > 0 || (p.mode & kRS))) && !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j)))
+        return;
       trace_ev(p, me, 2 + 2 * j);
       prev = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false);
       run(prev, j);

@@ -91,7 +91,8 @@ struct ddl_comm {
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int skip_rank = -1;
   bool use_tma = true;
-  bool use_steal = false;  // DDL_STEAL=1: per-CTA slices + work stealing (PATH 4)
+  bool use_steal = false;
+  bool use_stream = false;  // DDL_STREAM=1: no inner phase barriers, per-chunk progress (PATH 5)  // DDL_STEAL=1: per-CTA slices + work stealing (PATH 4)
   bool use_dyn = false;  // DDL_DYN=1: rank-level barriers + dynamic chunks (measured slower)
   int gpu_share = 1;
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)  // ranks sharing this GPU (loopback: P; in-process test groups: P)
@@ -130,6 +131,7 @@ void apply_env(ddl_comm* c) {
   c->use_tma = env_size("DDL_NO_TMA", 0) == 0;
   c->use_dyn = env_size("DDL_DYN", 0) != 0;
   c->use_steal = env_size("DDL_STEAL", 0) != 0;
+  c->use_stream = env_size("DDL_STREAM", 0) != 0;
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
@@ -150,7 +152,8 @@ ddl_result_t common_init(ddl_comm* c, int nranks, const int* dims, int ndims, in
   DDL_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
   c->cmax = c->num_sms * 4;
   const size_t words = (size_t)c->cmax * (1 + (size_t)kNumSlots * nranks) + kRankStateWords +
-                       16 + 2 * (size_t)kNumSlots * c->cmax;  // + steal counters
+                       16 + 2 * (size_t)kNumSlots * c->cmax +  // + steal counters
+                       2 + 2 * (size_t)kNumSlots * c->cmax;    // + streaming progress words
   c->flags_bytes = (words * 4 + 65535) / 65536 * 65536;
   apply_env(c);
   if (env_size("DDL_TRACE", 0)) {
@@ -175,6 +178,7 @@ struct Plan {
 
 template <typename T>
 const void* hier_fn(int path) {
+  if (path == 5) return (const void*)ddl_hier_kernel<T, 5>;
   if (path == 4) return (const void*)ddl_hier_kernel<T, 4>;
   if (path == 3) return (const void*)ddl_dyn_kernel<T>;
   if (path == 2) return (const void*)ddl_hier_kernel<T, 2>;
@@ -221,7 +225,7 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
   pl.vec = vec;
   const int w = elem_size(dt);
   const uint64_t W = vec ? 16 / w : 1;
-  pl.path = !vec ? 0 : (c->use_tma ? (c->use_dyn ? 3 : (c->use_steal ? 4 : 2)) : 1);
+  pl.path = !vec ? 0 : (c->use_tma ? (c->use_dyn ? 3 : (c->use_steal ? 4 : (c->use_stream ? 5 : 2))) : 1);
   int cap = cap_per_rank(c, hier_fn_dt(dt, pl.path), hier_smem(pl.path));
   if (pl.path >= 2 && q * w < c->tma_min_slice_bytes * (uint64_t)cap) {
     // small per-CTA slices: the register-staged path has lower per-phase latency
@@ -280,6 +284,7 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
   p.timeout_ns = c->timeout_ns;
   p.err = c->err;
   p.trace = c->trace;
+  p.stream_every = (int)(env_size("DDL_STREAM_EVERY", 1) ? env_size("DDL_STREAM_EVERY", 1) : 1);
   for (int r = 0; r < c->P; ++r) p.flags[r] = c->flags_of(r);
   return p;
 }

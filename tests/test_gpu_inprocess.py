@@ -36,11 +36,27 @@ def _short_timeout():
         os.environ["DDL_TIMEOUT_MS"] = old
 
 
-def group(P, dims):
-    key = (P, tuple(dims))
+def group(P, dims, env=None):
+    """env: extra DDL_* settings read at init (e.g. force the TMA-staged path)."""
+    key = (P, tuple(dims), tuple(sorted((env or {}).items())))
     if key not in _G:
-        _G[key] = ddl.InProcessGroup(P, list(dims), max_bytes=64 << 20)
+        old = {k: os.environ.get(k) for k in (env or {})}
+        os.environ.update(env or {})
+        try:
+            _G[key] = ddl.InProcessGroup(P, list(dims), max_bytes=64 << 20)
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
     return _G[key]
+
+
+# every hierarchical kernel variant of the multi-process launch path
+VARIANTS = {"default": None, "tma": {"DDL_TMA_MIN_SLICE_BYTES": "0"},
+            "stream": {"DDL_STREAM": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"},
+            "steal": {"DDL_STEAL": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"}}
 
 
 CASES = [(2, [2]), (4, [2, 2]), (4, [4]), (8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (6, [3, 2])]
@@ -49,9 +65,12 @@ IDS = [f"P{P}-{'x'.join(map(str, d))}" for P, d in CASES]
 
 @pytest.mark.parametrize("P,dims", CASES, ids=IDS)
 @pytest.mark.parametrize("algo", [ddl.ALGO_HIER, ddl.ALGO_ONESHOT], ids=["hier", "oneshot"])
-def test_allreduce_zero_copy_and_staged(P, dims, algo):
-    g = group(P, dims)
-    g.set_algo(algo, 1 << 40)
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_allreduce_zero_copy_and_staged(P, dims, algo, variant):
+    if algo == ddl.ALGO_ONESHOT and variant != "default":
+        pytest.skip("variants only change the hierarchical kernel")
+    g = group(P, dims, VARIANTS[variant])
+    g.set_algo(algo, 1 << 40 if algo == ddl.ALGO_ONESHOT else 0)
     for dtype in ("int32", "float32", "bfloat16"):
         for op in (["sum"] if dtype == "int32" else ["sum", "avg"]):
             for n in (1, 1000, 40_003, 300_001):
@@ -74,8 +93,9 @@ def test_allreduce_zero_copy_and_staged(P, dims, algo):
 
 
 @pytest.mark.parametrize("P,dims", CASES, ids=IDS)
-def test_reduce_scatter_allgather_staged(P, dims):
-    g = group(P, dims)
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_reduce_scatter_allgather_staged(P, dims, variant):
+    g = group(P, dims, VARIANTS[variant])
     for recv in (96, 1001, 50_000):
         for dtype in ("int32", "float32", "bfloat16"):
             op = "sum" if dtype == "int32" else "avg"

@@ -22,13 +22,14 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, env):
     import torch.distributed as dist
     import oracle
     import synthetic_inputs as si
     from gpu_util import to_dev, to_host, same_bits
     from paper_1811_12174_b200 import ddl
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), DDL_TIMEOUT_MS="20000")
+    os.environ.update(env)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     res = {}
@@ -55,12 +56,13 @@ def _rank_main(rank, world, port, q):
 
 
 @pytest.mark.timeout(240)
-def test_two_processes_ipc_one_gpu():
+@pytest.mark.parametrize("env", [{}, {"DDL_TMA_MIN_SLICE_BYTES": "0"}], ids=["default", "tma"])
+def test_two_processes_ipc_one_gpu(env):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, env)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}

@@ -255,7 +255,8 @@ def test_int32_bitmask_256MiB_closed_form():
 
 
 # ------------------------------------------------------------------ alternative kernel paths
-PATH_ENVS = {"steal": "DDL_STEAL", "dyn": "DDL_DYN", "ldg": "DDL_NO_TMA", "tma-all": "DDL_TMA_MIN_SLICE_BYTES"}
+PATH_ENVS = {"steal": "DDL_STEAL", "dyn": "DDL_DYN", "ldg": "DDL_NO_TMA", "tma-all": "DDL_TMA_MIN_SLICE_BYTES",
+             "stream": "DDL_STREAM"}
 
 
 @pytest.mark.parametrize("path", sorted(PATH_ENVS))
