@@ -587,6 +587,19 @@ __device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t 
                ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// Bulk store shared -> global (async proxy), grouped per thread.
+__device__ __forceinline__ void tma_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {  // sources of all my bulk stores read
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {  // all my bulk stores performed
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 // Make data that generic-proxy stores (this CTA's or a peer's, acquired through a device
 // barrier) visible to this thread's subsequent async-proxy (bulk copy) reads.
 __device__ __forceinline__ void fence_proxy_async_global() {
@@ -685,13 +698,19 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
         }
         st_vec(pd + (size_t)i * 16, pack<T>(acc));
       }
-    } else {
-      for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x)
-        st_vec(pd + (size_t)i * 16, *reinterpret_cast<const uint4*>(sbase + (size_t)i * 16));
+    } else if (threadIdx.x == 0) {
+      // copy: one bulk store from the stage (async proxy); the stage is reusable once the
+      // store has read it
+      tma_store(pd, sbase, bytes);
+      tma_store_wait_read();
     }
     coff += bytes;
     __syncthreads();  // every thread is done with stage st
     if (threadIdx.x == 0 && j + kStages < total) issue(sq + kStages);
+  }
+  if (x.kind != kPhRS && threadIdx.x == 0) {
+    tma_store_wait_all();        // the bulk stores are performed ...
+    fence_proxy_async_global();  // ... and ordered before this thread's generic operations
   }
   pp.seq += total;
   ragged_tails<T>(p, x, dst, s_units, s_srcs);
