@@ -45,7 +45,7 @@ DDL_HD int block_of(const Topo& t, int r, int d, int i) { return (r % t.G[d]) + 
 //   j = L           : before AG live[L-1], group live[L-1]
 //   j = L+1..2L-1   : before AG live[2L-1-j], that group (AG live[2L-j] done)
 //   j = 2L          : end, with EVERY group of r         (every peer finished reading r)
-// Returns the number of peers written to out (excluding r itself).
+// barrier_npeers / barrier_peer enumerate the peers (r itself excluded), one lane each.
 DDL_HD int barrier_dim(const Topo& t, int j) {
   const int L = t.nlive;
   if (j < L) return t.live[j];

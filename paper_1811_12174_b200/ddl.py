@@ -243,9 +243,24 @@ class Comm:
         return full[offset_bytes:offset_bytes + count * esz].view(dtype)
 
     def all_reduce(self, t, op: str = "sum", stream=None):
+        """In-place all-reduce.  A tensor inside the symmetric buffer is reduced zero-copy;
+        any other tensor larger than the staging workspace is reduced in workspace-sized
+        pieces (each element's result depends only on that element across ranks, so the
+        split never changes a bit)."""
         _require_cuda(t)
-        _check(_lib.ddl_allreduce(self.h, t.data_ptr(), t.numel(), DTYPE_CODES[dtype_name(t)], OP_CODES[op],
-                                  _stream(stream)), "ddl_allreduce")
+        dt = DTYPE_CODES[dtype_name(t)]
+        nbytes = t.numel() * t.element_size()
+        inside = self.buffer_ptr <= t.data_ptr() and t.data_ptr() + nbytes <= self.buffer_ptr + self.buffer_bytes
+        piece = (self.buffer_bytes // t.element_size()) // 256 * 256
+        if inside or nbytes <= self.buffer_bytes or piece == 0:
+            _check(_lib.ddl_allreduce(self.h, t.data_ptr(), t.numel(), dt, OP_CODES[op], _stream(stream)),
+                   "ddl_allreduce")
+            return t
+        flat = t.view(-1)
+        for lo in range(0, t.numel(), piece):
+            part = flat[lo:lo + piece]
+            _check(_lib.ddl_allreduce(self.h, part.data_ptr(), part.numel(), dt, OP_CODES[op], _stream(stream)),
+                   "ddl_allreduce")
         return t
 
     def reduce_scatter(self, out, inp, op: str = "sum", stream=None):

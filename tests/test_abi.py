@@ -194,3 +194,19 @@ def test_gloo_world2_bootstrap():
         assert res[r]["blob"] == bytes([0]) * 16 + bytes([1]) * 16
         assert sorted(sum(res[r]["owned"], [])) == list(range(world))
         assert res[r]["mismatch"]
+
+
+def test_plain_c_client(tmp_path):
+    """include/ddl.h compiles as C99 and a C program links and runs against libddl.so."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    exe = tmp_path / "c_abi_smoke"
+    libdir = os.path.join(ROOT, "paper_1811_12174_b200")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c_abi_smoke.c"), "-L", libdir, "-lddl",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "c_abi_smoke ok" in r.stdout
