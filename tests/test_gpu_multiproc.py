@@ -47,6 +47,13 @@ def _rank_main(rank, world, port, q, env):
             comm.all_reduce(st, op)
             torch.cuda.synchronize()
             res[dtype] = (same_bits(to_host(zc), want), same_bits(to_host(st), want))
+        # staged message larger than the workspace: reduced in pieces (ddl.Comm.all_reduce)
+        big = si.rank_buffers("float32", "normal", 6_000_001, world, seed=5)
+        want = oracle.allreduce_sampled(big, [world], "float32", "avg", np.arange(0, 6_000_001, 997))
+        tb = to_dev(big[rank], "float32")
+        comm.all_reduce(tb, "avg")
+        torch.cuda.synchronize()
+        res["big"] = (same_bits(to_host(tb)[::997], want),)
         res["err"] = comm.async_error()
         comm.finalize()
     except Exception as e:  # report, don't hang the parent
@@ -78,5 +85,5 @@ def test_two_processes_ipc_one_gpu(env):
     for r in range(world):
         assert "exc" not in out[r], out[r]
         assert out[r]["err"] == 0
-        for dtype in ("float32", "int32", "bfloat16"):
-            assert out[r][dtype] == (True, True), (r, dtype)
+        for dtype in ("float32", "int32", "bfloat16", "big"):
+            assert all(out[r][dtype]), (r, dtype)
