@@ -119,8 +119,22 @@ ddl_result_t ddl_connect(ddl_comm_t comm, const void* all_handles /* nranks * ha
  * inside it, at the SAME offset on every rank, reads peers' data in place (no staging). */
 ddl_result_t ddl_buffer(ddl_comm_t comm, void** dev_ptr, size_t* bytes);
 
-/* In-place all-reduce of buf[0, count).  buf inside ddl_buffer(): zero-copy; any other
- * device buffer: staged through the workspace (count * size <= max_bytes). */
+/* Registered buffers (SURVEY 8(b) ddl_register): persistent user buffers -- e.g. DDP's
+ * gradient buckets -- made zero-copy.  Collective: every rank calls
+ * ddl_register_export(ptr, bytes) on ITS buffer (equal bytes on every rank), the caller
+ * all-gathers the ddl_reg_handle_size() blobs in rank order, and every rank calls
+ * ddl_register_connect(ptr, blobs) -> reg_id.  Afterwards an all-reduce on any sub-range
+ * of the buffer, at the SAME offset on every rank, reads peers in place.  The buffer must
+ * come from cudaMalloc (or torch's default caching allocator) and outlive the
+ * registration; ddl_deregister (or ddl_finalize) unmaps it.  At most 64 registrations. */
+size_t ddl_reg_handle_size(void);
+ddl_result_t ddl_register_export(ddl_comm_t comm, void* ptr, size_t bytes, void* handle_out);
+ddl_result_t ddl_register_connect(ddl_comm_t comm, void* ptr, const void* all_handles, int* reg_id);
+ddl_result_t ddl_deregister(ddl_comm_t comm, int reg_id);
+
+/* In-place all-reduce of buf[0, count).  buf inside ddl_buffer() or a registered buffer:
+ * zero-copy; any other device buffer: staged through the workspace (count * size <=
+ * max_bytes). */
 ddl_result_t ddl_allreduce(ddl_comm_t comm, void* buf, size_t count, ddl_dtype_t dtype,
                            ddl_op_t op, void* stream);
 
@@ -167,6 +181,10 @@ ddl_result_t ddl_debug_trace(ddl_comm_t comm, void* host_out, size_t bytes);
  * path (per-rank launches on the caller's streams, .sys-scope flags, zero-copy and staged
  * buffers) with the ranks' kernels co-resident on one GPU (CTA budget divided by nranks). */
 ddl_result_t ddl_debug_connect_local(ddl_comm_t* comms, int nranks);
+
+/* Test hook: register ptrs[r] (bytes each) for the in-process communicators comms[r]
+ * (see ddl_debug_connect_local) without cudaIpc; same reg_id on every rank. */
+ddl_result_t ddl_debug_register_local(ddl_comm_t* comms, void* const* ptrs, size_t bytes, int nranks, int* reg_id);
 
 /* Collective teardown: every rank must have finished all calls (host barrier first).
  * Unmaps peers, frees the workspace, destroys the handle.  NULL is a no-op. */

@@ -11,6 +11,7 @@
 #include <new>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "ddl.h"
 #include "ddl_device.cuh"
@@ -59,6 +60,34 @@ struct Handle {  // exported per rank, all-gathered by the caller
   cudaIpcMemHandle_t ipc;
 };
 
+struct RegHandle {  // exported per rank by ddl_register_export, all-gathered by the caller
+  uint32_t magic;
+  int32_t rank;
+  uint64_t bytes;
+  uint64_t offset;  // registered pointer - base of its cudaMalloc allocation
+  cudaIpcMemHandle_t ipc;
+};
+constexpr uint32_t kRegMagic = 0xDD1A4E61u;
+
+typedef int (*CuMemGetAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+// Base of the cudaMalloc allocation containing ptr (driver entry point, no libcuda link).
+cudaError_t alloc_base(const void* ptr, char** base) {
+  static CuMemGetAddressRange fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !f) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    fn = reinterpret_cast<CuMemGetAddressRange>(f);
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)(uintptr_t)ptr) != 0) return cudaErrorInvalidValue;
+  *base = reinterpret_cast<char*>(b);
+  return cudaSuccess;
+}
+
 }  // namespace
 
 struct ddl_comm {
@@ -91,11 +120,11 @@ struct ddl_comm {
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int skip_rank = -1;
   bool use_tma = true;
-  bool use_steal = false;
-  bool use_stream = false;  // DDL_STREAM=1: no inner phase barriers, per-chunk progress (PATH 5)  // DDL_STEAL=1: per-CTA slices + work stealing (PATH 4)
-  bool use_dyn = false;  // DDL_DYN=1: rank-level barriers + dynamic chunks (measured slower)
-  int gpu_share = 1;
-  uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)  // ranks sharing this GPU (loopback: P; in-process test groups: P)
+  bool use_steal = false;  // DDL_STEAL=1: per-CTA slices + work stealing (PATH 4)
+  bool use_stream = false;  // DDL_STREAM=1: no inner phase barriers, per-chunk progress (PATH 5)
+  bool use_dyn = false;     // DDL_DYN=1: rank-level barriers + dynamic chunks (measured slower)
+  int gpu_share = 1;        // ranks sharing this GPU (loopback: P; in-process test groups: P)
+  uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
 
   uint32_t* flags_of(int r) const {
@@ -103,6 +132,24 @@ struct ddl_comm {
     return reinterpret_cast<uint32_t*>(r == rank ? alloc : peer_base[r]);
   }
   char* sym_of(int r) const { return (r == rank ? alloc : peer_base[r]) + flags_bytes; }
+  // registered user buffers (ddl_register_*): zero-copy at the same offset on every rank
+  struct Reg {
+    bool used = false;
+    char* local = nullptr;
+    size_t bytes = 0;
+    char* peer[kMaxRanks] = {};      // every rank's registered pointer, as mapped here
+    char* mapped[kMaxRanks] = {};    // IPC mapping bases this registration opened (to close)
+  };
+  static constexpr int kMaxRegs = 64;
+  Reg regs[kMaxRegs];
+  // IPC mappings of peer allocations, shared by registrations of the same allocation
+  struct Mapping {
+    int rank;
+    cudaIpcMemHandle_t h;
+    char* base;
+    int refs;
+  };
+  std::vector<Mapping> maps;
   char* stage_of(int r) const { return (r == rank ? alloc : peer_base[r]) + flags_bytes + max_bytes; }
 };
 
@@ -523,7 +570,13 @@ ddl_result_t ddl_allreduce(ddl_comm_t c, void* buf, size_t count, ddl_dtype_t dt
   if (!buf || !aligned16(buf)) return DDL_ERR_INVALID_ARGUMENT;
   const size_t bytes = count * elem_size(dt);
   char* sym = c->alloc + c->flags_bytes;
-  const bool zero_copy = (char*)buf >= sym && (char*)buf + bytes <= sym + c->max_bytes;
+  const bool in_sym = (char*)buf >= sym && (char*)buf + bytes <= sym + c->max_bytes;
+  const ddl_comm::Reg* reg = nullptr;
+  for (int k = 0; k < ddl_comm::kMaxRegs && !in_sym && !reg; ++k) {
+    const ddl_comm::Reg& g = c->regs[k];
+    if (g.used && (char*)buf >= g.local && (char*)buf + bytes <= g.local + g.bytes) reg = &g;
+  }
+  const bool zero_copy = in_sym || reg;
   if (!zero_copy && bytes > c->max_bytes) return DDL_ERR_TOO_LARGE;
   DDL_CUDA(cudaSetDevice(c->device));
   KParams p = base_params(c, count, op);
@@ -532,9 +585,9 @@ ddl_result_t ddl_allreduce(ddl_comm_t c, void* buf, size_t count, ddl_dtype_t dt
   if (!one) pl = plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true);
   p.q = pl.q;
   p.slice = pl.slice;
-  const size_t off = zero_copy ? (size_t)((char*)buf - sym) : 0;
+  const size_t off = in_sym ? (size_t)((char*)buf - sym) : reg ? (size_t)((char*)buf - reg->local) : 0;
   for (int m = 0; m < c->P; ++m) {
-    char* base = zero_copy ? c->sym_of(m) + off : c->stage_of(m);
+    char* base = in_sym ? c->sym_of(m) + off : reg ? reg->peer[m] + off : c->stage_of(m);
     p.in[m] = base;
     p.work[m] = base;
     p.out[m] = base;
@@ -673,10 +726,120 @@ ddl_result_t ddl_debug_connect_local(ddl_comm_t* comms, int nranks) {
   return DDL_SUCCESS;
 }
 
+size_t ddl_reg_handle_size(void) { return sizeof(RegHandle); }
+
+ddl_result_t ddl_register_export(ddl_comm_t c, void* ptr, size_t bytes, void* out) {
+  if (!c || !ptr || !out || c->loopback || bytes == 0 || !aligned16(ptr)) return DDL_ERR_INVALID_ARGUMENT;
+  DDL_CUDA(cudaSetDevice(c->device));
+  char* base = nullptr;
+  DDL_CUDA(alloc_base(ptr, &base));
+  RegHandle h;
+  std::memset(&h, 0, sizeof(h));
+  h.magic = kRegMagic;
+  h.rank = c->rank;
+  h.bytes = bytes;
+  h.offset = (uint64_t)((char*)ptr - base);
+  DDL_CUDA(cudaIpcGetMemHandle(&h.ipc, base));
+  std::memcpy(out, &h, sizeof(h));
+  return DDL_SUCCESS;
+}
+
+static int free_reg(ddl_comm* c) {
+  for (int k = 0; k < ddl_comm::kMaxRegs; ++k)
+    if (!c->regs[k].used) return k;
+  return -1;
+}
+
+ddl_result_t ddl_register_connect(ddl_comm_t c, void* ptr, const void* all_handles, int* reg_id) {
+  if (!c || !ptr || !all_handles || !reg_id || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  const RegHandle* hs = static_cast<const RegHandle*>(all_handles);
+  for (int m = 0; m < c->P; ++m)
+    if (hs[m].magic != kRegMagic || hs[m].rank != m) return DDL_ERR_INVALID_ARGUMENT;
+  for (int m = 0; m < c->P; ++m)
+    if (hs[m].bytes != hs[c->rank].bytes) return DDL_ERR_MISMATCH;
+  const int k = free_reg(c);
+  if (k < 0) return DDL_ERR_UNSUPPORTED;
+  DDL_CUDA(cudaSetDevice(c->device));
+  ddl_comm::Reg g;
+  g.local = static_cast<char*>(ptr);
+  g.bytes = hs[c->rank].bytes;
+  for (int m = 0; m < c->P; ++m) {
+    if (m == c->rank) {
+      g.peer[m] = g.local;
+      continue;
+    }
+    char* base = nullptr;
+    for (auto& mp : c->maps)
+      if (mp.rank == m && !std::memcmp(&mp.h, &hs[m].ipc, sizeof(cudaIpcMemHandle_t))) {
+        base = mp.base;
+        ++mp.refs;
+      }
+    if (!base) {
+      void* v = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&v, hs[m].ipc, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle (register)");
+      base = static_cast<char*>(v);
+      c->maps.push_back(ddl_comm::Mapping{m, hs[m].ipc, base, 1});
+    }
+    g.mapped[m] = base;
+    g.peer[m] = base + hs[m].offset;
+  }
+  g.used = true;
+  c->regs[k] = g;
+  *reg_id = k;
+  return DDL_SUCCESS;
+}
+
+static void release_reg(ddl_comm* c, int k) {
+  ddl_comm::Reg& g = c->regs[k];
+  for (int m = 0; m < kMaxRanks; ++m) {
+    if (!g.mapped[m]) continue;
+    for (size_t i = 0; i < c->maps.size(); ++i)
+      if (c->maps[i].base == g.mapped[m] && c->maps[i].rank == m && --c->maps[i].refs == 0) {
+        cudaIpcCloseMemHandle(c->maps[i].base);
+        c->maps.erase(c->maps.begin() + i);
+        break;
+      }
+  }
+  g = ddl_comm::Reg();
+}
+
+ddl_result_t ddl_deregister(ddl_comm_t c, int reg_id) {
+  if (!c || reg_id < 0 || reg_id >= ddl_comm::kMaxRegs || !c->regs[reg_id].used) return DDL_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  release_reg(c, reg_id);
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_debug_register_local(ddl_comm_t* comms, void* const* ptrs, size_t bytes, int nranks, int* reg_id) {
+  if (!comms || !ptrs || !reg_id || nranks < 1 || nranks > kMaxRanks || bytes == 0) return DDL_ERR_INVALID_ARGUMENT;
+  int k = -1;
+  for (int kk = 0; kk < ddl_comm::kMaxRegs && k < 0; ++kk) {
+    bool ok = true;
+    for (int r = 0; r < nranks; ++r) ok = ok && !comms[r]->regs[kk].used;
+    if (ok) k = kk;
+  }
+  if (k < 0) return DDL_ERR_UNSUPPORTED;
+  for (int r = 0; r < nranks; ++r) {
+    if (!ptrs[r] || !aligned16(ptrs[r])) return DDL_ERR_INVALID_ARGUMENT;
+    ddl_comm::Reg& g = comms[r]->regs[k];
+    g = ddl_comm::Reg();
+    g.used = true;
+    g.local = static_cast<char*>(ptrs[r]);
+    g.bytes = bytes;
+    for (int m = 0; m < nranks; ++m) g.peer[m] = static_cast<char*>(ptrs[m]);
+  }
+  *reg_id = k;
+  return DDL_SUCCESS;
+}
+
 ddl_result_t ddl_finalize(ddl_comm_t c) {
   if (!c) return DDL_SUCCESS;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  for (int k = 0; k < ddl_comm::kMaxRegs; ++k)
+    if (c->regs[k].used) release_reg(c, k);
   for (int m = 0; m < kMaxRanks; ++m)
     if (c->peer_mapped[m]) cudaIpcCloseMemHandle(c->peer_base[m]);
   if (c->alloc) cudaFree(c->alloc);

@@ -76,6 +76,11 @@ def _load() -> ctypes.CDLL:
         "ddl_ctas_for": (c_int, [c_void, c_size, c_int]),
         "ddl_debug_skip_rank": (c_int, [c_void, c_int]),
         "ddl_debug_connect_local": (c_int, [pp, c_int]),
+        "ddl_reg_handle_size": (c_size, []),
+        "ddl_register_export": (c_int, [c_void, c_void, c_size, c_void]),
+        "ddl_register_connect": (c_int, [c_void, c_void, c_void, ip]),
+        "ddl_deregister": (c_int, [c_void, c_int]),
+        "ddl_debug_register_local": (c_int, [pp, pp, c_size, c_int, ip]),
         "ddl_debug_trace": (c_int, [c_void, c_void, c_size]),
         "ddl_finalize": (c_int, [c_void]),
         "ddl_loopback_init": (c_int, [pp, c_int, ip, c_int, c_int]),
@@ -263,6 +268,24 @@ class Comm:
                    "ddl_allreduce")
         return t
 
+    def register(self, t) -> int:
+        """Collective: register a persistent device tensor (same size on every rank) so that
+        all-reduces on it -- or on a view at the same offset on every rank -- are zero-copy."""
+        import torch.distributed as dist
+        _require_cuda(t)
+        nbytes = t.numel() * t.element_size()
+        blob = ctypes.create_string_buffer(_lib.ddl_reg_handle_size())
+        _check(_lib.ddl_register_export(self.h, t.data_ptr(), nbytes, blob), "ddl_register_export")
+        allb = [None] * self.nranks
+        dist.all_gather_object(allb, bytes(blob.raw), group=self.group)
+        joined = ctypes.create_string_buffer(b"".join(allb), len(blob.raw) * self.nranks)
+        rid = ctypes.c_int()
+        _check(_lib.ddl_register_connect(self.h, t.data_ptr(), joined, ctypes.byref(rid)), "ddl_register_connect")
+        return rid.value
+
+    def deregister(self, reg_id: int) -> None:
+        _check(_lib.ddl_deregister(self.h, reg_id), "ddl_deregister")
+
     def reduce_scatter(self, out, inp, op: str = "sum", stream=None):
         _require_cuda(out)
         _require_cuda(inp)
@@ -420,6 +443,15 @@ class InProcessGroup:
     def buffer(self, r: int, count: int, dtype, offset_bytes: int = 0):
         esz = _torch().tensor([], dtype=dtype).element_size()
         return self.buf[r][offset_bytes:offset_bytes + count * esz].view(dtype)
+
+    def register(self, tensors) -> int:
+        """Register one tensor per rank (equal sizes) for zero-copy all-reduces."""
+        rid = ctypes.c_int()
+        nbytes = tensors[0].numel() * tensors[0].element_size()
+        _check(_lib.ddl_debug_register_local(_ptrs([h.value for h in self.hs]),
+                                             _ptrs([t.data_ptr() for t in tensors]), nbytes, self.nranks,
+                                             ctypes.byref(rid)), "ddl_debug_register_local")
+        return rid.value
 
     def _each(self, fn):
         torch = _torch()

@@ -20,8 +20,16 @@ from .ddl import Comm
 
 def ddl_allreduce_hook(state: Comm, bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
     """DDP comm hook: average the bucket with DDL's all-reduce (enqueued on the current
-    stream, so DDP's copy-back is stream-ordered after it)."""
+    stream, so DDP's copy-back is stream-ordered after it).  Each bucket buffer is
+    registered with DDL the first time it is seen (a collective every rank performs at the
+    same bucket), so every later step all-reduces it zero-copy instead of staging it
+    through the workspace.  DDP's buffers are persistent (they change only if DDP rebuilds
+    its buckets, which then registers the new ones)."""
     buf = bucket.buffer()
+    regs = state.__dict__.setdefault("_ddp_registered", {})
+    key = (buf.data_ptr(), buf.numel() * buf.element_size())
+    if key not in regs:
+        regs[key] = state.register(buf)
     state.all_reduce(buf, "avg")
     fut = torch.futures.Future()
     fut.set_result(buf)

@@ -138,3 +138,24 @@ def test_many_calls_mixed_paths():
         g.all_reduce(ts)
         torch.cuda.synchronize()
         assert all(np.array_equal(to_host(t), want) for t in ts), (i, n)
+
+
+@pytest.mark.parametrize("variant", ["default", "tma"])
+def test_registered_buffers_zero_copy(variant):
+    """ddl_register (in-process hook): all-reduces on registered tensors -- and on views at
+    the same offset on every rank -- read peers in place and match the oracle."""
+    P, dims = 4, [2, 2]
+    g = group(P, dims, VARIANTS[variant])
+    n = 2_000_003
+    regs = [torch.zeros(n + 64, device="cuda") for _ in range(P)]
+    g.register(regs)
+    for off, cnt in ((0, n), (64, 500_000), (16, 1)):
+        bufs = si.rank_buffers("float32", "normal", cnt, P, seed=off + cnt)
+        views = [regs[r][off:off + cnt] for r in range(P)]
+        for r in range(P):
+            views[r].copy_(to_dev(bufs[r], "float32"))
+        g.all_reduce(views, "avg")
+        torch.cuda.synchronize()
+        want = oracle.allreduce(bufs, dims, "float32", "avg")
+        for r in range(P):
+            assert same_bits(to_host(views[r]), want[r]), (off, cnt, r)

@@ -54,6 +54,15 @@ def _rank_main(rank, world, port, q, env):
         comm.all_reduce(tb, "avg")
         torch.cuda.synchronize()
         res["big"] = (same_bits(to_host(tb)[::997], want),)
+        # registered (cudaIpc-mapped) user buffer: zero-copy all-reduce on a view
+        reg = torch.zeros(300_000, device="cuda")
+        comm.register(reg)
+        rb = si.rank_buffers("float32", "normal", 250_000, world, seed=9)
+        view = reg[1024:1024 + 250_000]
+        view.copy_(to_dev(rb[rank], "float32"))
+        comm.all_reduce(view, "avg")
+        torch.cuda.synchronize()
+        res["registered"] = (same_bits(to_host(view), oracle.allreduce(rb, [world], "float32", "avg")[rank]),)
         res["err"] = comm.async_error()
         comm.finalize()
     except Exception as e:  # report, don't hang the parent
@@ -85,5 +94,5 @@ def test_two_processes_ipc_one_gpu(env):
     for r in range(world):
         assert "exc" not in out[r], out[r]
         assert out[r]["err"] == 0
-        for dtype in ("float32", "int32", "bfloat16", "big"):
+        for dtype in ("float32", "int32", "bfloat16", "big", "registered"):
             assert all(out[r][dtype]), (r, dtype)
