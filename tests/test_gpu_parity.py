@@ -316,3 +316,33 @@ def test_randomized_instances():
         got = run_allreduce(lb, bufs, dtype, op)
         for r in range(P):
             assert same_bits(got[r], want[r]), (case, P, dims, dtype, op, n, algo, r)
+
+
+@pytest.mark.parametrize("algo", [ddl.ALGO_HIER, ddl.ALGO_ONESHOT], ids=["hier", "oneshot"])
+def test_cuda_graph_capture_replay(algo):
+    """The call epoch lives on the device, so a captured all-reduce can be replayed: every
+    replay on fresh inputs matches the oracle (graph-capturable calls)."""
+    P, dims, n = 8, [4, 2], 100_003
+    lb = ddl.Loopback(P, dims)
+    lb.set_algo(algo, 1 << 40)
+    bufs = [torch.zeros(n, device="cuda") for _ in range(P)]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            lb.all_reduce(bufs, "avg")
+            lb.all_reduce(bufs, "sum")   # two calls in one graph
+    torch.cuda.synchronize()
+    for it in range(4):
+        host = si.rank_buffers("float32", "normal", n, P, seed=50 + it)
+        for r in range(P):
+            bufs[r].copy_(to_dev(host[r], "float32"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert lb.async_error() == ddl.SUCCESS
+        mid = oracle.allreduce(host, dims, "float32", "avg")
+        want = oracle.allreduce(mid, dims, "float32", "sum")
+        for r in range(P):
+            assert same_bits(to_host(bufs[r]), want[r]), (it, r)
+    lb.finalize()
