@@ -140,12 +140,14 @@ ddl_result_t ddl_allreduce(ddl_comm_t comm, void* buf, size_t count, ddl_dtype_t
 
 /* NCCL layout: sendbuf holds nranks * recvcount elements; rank r receives elements
  * [r*recvcount, (r+1)*recvcount) of the reduced vector.  sendbuf is not modified.
- * Staged through the workspace: nranks * recvcount * size <= max_bytes. */
+ * The partial sums live in the workspace: nranks * recvcount * size <= max_bytes.  A
+ * sendbuf in the symmetric / a registered buffer is read in place (no copy-in). */
 ddl_result_t ddl_reduce_scatter(ddl_comm_t comm, const void* sendbuf, void* recvbuf, size_t recvcount,
                                 ddl_dtype_t dtype, ddl_op_t op, void* stream);
 
 /* Rank r's sendcount elements land at [r*sendcount, (r+1)*sendcount) of every rank's
- * recvbuf (nranks * sendcount elements).  Staged through the workspace. */
+ * recvbuf (nranks * sendcount elements).  A recvbuf in the symmetric / a registered buffer
+ * is gathered into in place; otherwise staged through the workspace (<= max_bytes). */
 ddl_result_t ddl_allgather(ddl_comm_t comm, const void* sendbuf, void* recvbuf, size_t sendcount,
                            ddl_dtype_t dtype, void* stream);
 

@@ -363,6 +363,25 @@ ddl_result_t check_common(const ddl_comm* c, ddl_dtype_t dt, ddl_op_t op) {
   return DDL_SUCCESS;
 }
 
+// If [ptr, ptr+bytes) lies in the symmetric buffer or in a registered buffer, fill peer[m]
+// with every rank's address of the same offset and return true (zero-copy).
+bool zero_copy_peers(const ddl_comm* c, const void* ptr, size_t bytes, const char** peer) {
+  const char* q = static_cast<const char*>(ptr);
+  const char* sym = c->alloc + c->flags_bytes;
+  if (q >= sym && q + bytes <= sym + c->max_bytes) {
+    for (int m = 0; m < c->P; ++m) peer[m] = c->sym_of(m) + (q - sym);
+    return true;
+  }
+  for (int k = 0; k < ddl_comm::kMaxRegs; ++k) {
+    const ddl_comm::Reg& g = c->regs[k];
+    if (g.used && q >= g.local && q + bytes <= g.local + g.bytes) {
+      for (int m = 0; m < c->P; ++m) peer[m] = g.peer[m] + (q - g.local);
+      return true;
+    }
+  }
+  return false;
+}
+
 // Local copy (P = 1 reduce-scatter / allgather) through the local-reduce kernel.
 ddl_result_t local_copy(const void* src, void* dst, size_t count, ddl_dtype_t dt, void* stream) {
   if (src == dst || count == 0) return DDL_SUCCESS;
@@ -628,6 +647,13 @@ ddl_result_t ddl_reduce_scatter(ddl_comm_t c, const void* sendbuf, void* recvbuf
   p.cin[c->rank] = sendbuf;
   p.out[c->rank] = static_cast<char*>(recvbuf) - (ptrdiff_t)c->rank * (ptrdiff_t)(recvcount * w);
   p.mode = kCinAll | kRS;
+  // zero-copy input: peers' phase-0 reads come straight from their (symmetric or
+  // registered) send buffers; the partials still go to the staging workspace (send is const)
+  const char* sp[kMaxRanks];
+  if (zero_copy_peers(c, sendbuf, n * w, sp)) {
+    for (int m = 0; m < c->P; ++m) p.in[m] = sp[m];
+    p.mode = kRS;
+  }
   return launch(c, p, pl, dt, stream);
 }
 
@@ -641,7 +667,8 @@ ddl_result_t ddl_allgather(ddl_comm_t c, const void* sendbuf, void* recvbuf, siz
   const int w = elem_size(dt);
   if (c->P == 1) return local_copy(sendbuf, recvbuf, sendcount, dt, stream);
   const size_t n = sendcount * (size_t)c->P;
-  if (n * w > c->max_bytes) return DDL_ERR_TOO_LARGE;
+  const char* chk[kMaxRanks];
+  if (n * w > c->max_bytes && !zero_copy_peers(c, recvbuf, n * w, chk)) return DDL_ERR_TOO_LARGE;
   DDL_CUDA(cudaSetDevice(c->device));
   const bool vec = (sendcount * w) % 16 == 0;
   Plan pl = plan_hier(c, n, sendcount, dt, vec);
@@ -652,6 +679,12 @@ ddl_result_t ddl_allgather(ddl_comm_t c, const void* sendbuf, void* recvbuf, siz
   p.cin[c->rank] = sendbuf;
   p.cout[c->rank] = recvbuf;
   p.mode = kCinOwn | kAG | kCoutAll;
+  // zero-copy output: gather straight into every rank's (symmetric or registered) recvbuf
+  const char* rp[kMaxRanks];
+  if (zero_copy_peers(c, recvbuf, n * w, rp)) {
+    for (int m = 0; m < c->P; ++m) p.work[m] = const_cast<char*>(rp[m]);
+    p.mode = kCinOwn | kAG;
+  }
   return launch(c, p, pl, dt, stream);
 }
 

@@ -159,3 +159,35 @@ def test_registered_buffers_zero_copy(variant):
         want = oracle.allreduce(bufs, dims, "float32", "avg")
         for r in range(P):
             assert same_bits(to_host(views[r]), want[r]), (off, cnt, r)
+
+
+@pytest.mark.parametrize("variant", ["default", "tma"])
+def test_zero_copy_reduce_scatter_allgather(variant):
+    """reduce_scatter reading registered send buffers in place, allgather writing registered
+    recv buffers in place (symmetric buffer too): bit-exact vs the oracle."""
+    P, dims, recv = 8, [4, 2], 70_000
+    g = group(P, dims, VARIANTS[variant])
+    send = [torch.empty(P * recv, device="cuda") for _ in range(P)]
+    g.register(send)
+    bufs = si.rank_buffers("float32", "normal", P * recv, P, seed=21)
+    for r in range(P):
+        send[r].copy_(to_dev(bufs[r], "float32"))
+    outs = [torch.empty(recv, device="cuda") for _ in range(P)]
+    g.reduce_scatter(outs, send, "avg")
+    torch.cuda.synchronize()
+    want = oracle.reduce_scatter(bufs, dims, "float32", "avg")
+    for r in range(P):
+        assert same_bits(to_host(outs[r]), want[r]), ("rs", r)
+        assert same_bits(to_host(send[r]), bufs[r])            # send untouched
+    # allgather into the symmetric buffer (zero-copy) and into a registered buffer
+    blocks = si.rank_buffers("float32", "normal", recv, P, seed=22)
+    wantg = oracle.allgather(blocks, dims, "float32")
+    sym = [g.buffer(r, P * recv, torch.float32, offset_bytes=1 << 20) for r in range(P)]
+    reg = [torch.empty(P * recv, device="cuda") for _ in range(P)]
+    g.register(reg)
+    for target in (sym, reg):
+        ins = [to_dev(b, "float32") for b in blocks]
+        g.all_gather(target, ins)
+        torch.cuda.synchronize()
+        for r in range(P):
+            assert same_bits(to_host(target[r]), wantg[r]), ("ag", r)
