@@ -46,6 +46,7 @@ struct KParams {
   Topo t;
   int rank;            // this process's rank (multi-process); loopback: me = blockIdx.y
   int loopback;
+  int gpu_scope;       // every rank on this GPU (loopback, in-process groups): .gpu-scope flags suffice
   int op;
   int cmax;            // CTA stride of the flag slots
   float scale;         // fl32(1/P) for avg
@@ -193,11 +194,11 @@ __device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int
   int fail = 0;
   if (threadIdx.x < np) {
     const int m = peer(threadIdx.x);
-    st_release(flag_slot(p, p.flags[m], slot, blockIdx.x, me), epoch, p.loopback);
+    st_release(flag_slot(p, p.flags[m], slot, blockIdx.x, me), epoch, p.gpu_scope);
     const uint32_t* f = flag_slot(p, p.flags[me], slot, blockIdx.x, m);
     uint64_t t0 = 0;
     uint32_t spins = 0;
-    while ((int32_t)(ld_acquire(f, p.loopback) - epoch) < 0) {
+    while ((int32_t)(ld_acquire(f, p.gpu_scope) - epoch) < 0) {
       if ((++spins & 1023u) == 0) {
         const uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
@@ -1105,7 +1106,7 @@ __device__ void stream_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& 
       const uint64_t* w = prog_word(p, s_nr[u][v], ph) + c;
       uint64_t t0 = 0;
       uint32_t spins = 0;
-      while (ld_acquire64(w, p.loopback) < (ehi | need)) {
+      while (ld_acquire64(w, p.gpu_scope) < (ehi | need)) {
         if ((++spins & 1023u) == 0) {
           const uint64_t now = globaltimer();
           if (t0 == 0) t0 = now;
@@ -1167,7 +1168,7 @@ __device__ void stream_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& 
         do {
           asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(got) : "r"(smem_u32(pp.stored)) : "memory");
         } while ((int32_t)(got - want) < 0);
-        if ((j + 1) % p.stream_every == 0 || j + 1 == total) st_release64(myprog, ehi | (j + 1), p.loopback);
+        if ((j + 1) % p.stream_every == 0 || j + 1 == total) st_release64(myprog, ehi | (j + 1), p.gpu_scope);
       }
     }
   }
@@ -1231,7 +1232,7 @@ __device__ void stream_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& 
     ragged_tails<T>(p, x, dst, s_units, s_srcs);
   }
   __syncthreads();
-  if (threadIdx.x == 32) st_release64(myprog, ehi | (total + 1), p.loopback);  // phase complete
+  if (threadIdx.x == 32) st_release64(myprog, ehi | (total + 1), p.gpu_scope);  // phase complete
 }
 
 // ------------------------------------------------------------------------ the hierarchical kernel
@@ -1366,7 +1367,7 @@ __device__ __forceinline__ void rank_arrive(const KParams& p, int me, int j, int
         const int np = barrier_npeers(p.t, slot);
         for (int l = 0; l <= np; ++l) {
           const int m = rank_barrier_member(p.t, me, slot, l);
-          st_release(rs_flag(rank_state(p, m), slot, me), epoch, p.loopback);
+          st_release(rs_flag(rank_state(p, m), slot, me), epoch, p.gpu_scope);
         }
       }
     }
@@ -1382,7 +1383,7 @@ __device__ __forceinline__ bool rank_wait(const KParams& p, int me, int slot, ui
     const uint32_t* f = rs_flag(rank_state(p, me), slot, m);
     uint64_t t0 = 0;
     uint32_t spins = 0;
-    while ((int32_t)(ld_acquire(f, p.loopback) - epoch) < 0) {
+    while ((int32_t)(ld_acquire(f, p.gpu_scope) - epoch) < 0) {
       if ((++spins & 1023u) == 0) {
         const uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;

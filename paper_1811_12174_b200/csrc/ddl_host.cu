@@ -323,6 +323,7 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
   p.t = c->topo;
   p.rank = c->rank;
   p.loopback = c->loopback ? 1 : 0;
+  p.gpu_scope = (c->gpu_share == c->P && !env_size("DDL_FORCE_SYS_SCOPE", 0)) ? 1 : 0;
   p.op = op;
   p.cmax = c->cmax;
   p.scale = 1.0f / (float)c->P;  // fl32(1/P)

@@ -15,8 +15,11 @@ ap.add_argument("--dims", default="2x4")
 ap.add_argument("--sizes", default="8196000,31502336")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--zero-copy", action="store_true")
+ap.add_argument("--graph", action="store_true", help="capture all ranks' launches in one CUDA graph")
+ap.add_argument("--algo", type=int, default=0)
 a = ap.parse_args()
 g = ddl.InProcessGroup(a.P, ddl.parse_dims(a.dims), max_bytes=1 << 30)
+g.set_algo(a.algo, 512 << 10)
 for S in [int(x) for x in a.sizes.split(",")]:
     n = S // 4
     if a.zero_copy:
@@ -29,12 +32,26 @@ for S in [int(x) for x in a.sizes.split(",")]:
         g.all_reduce(bufs, "avg")
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.iters):
-        g.all_reduce(bufs, "avg")
-    e1.record()
+    if a.graph:
+        cg = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(cg, stream=cs):
+                for _ in range(a.iters):
+                    g.all_reduce(bufs, "avg")
+        cg.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        cg.replay()
+        e1.record()
+    else:
+        e0.record()
+        for _ in range(a.iters):
+            g.all_reduce(bufs, "avg")
+        e1.record()
     torch.cuda.synchronize()
     assert g.async_error() == 0
     us = e0.elapsed_time(e1) * 1e3 / a.iters
-    print(f"inproc{'-zc' if a.zero_copy else '-staged'},{a.P},{a.dims},{S},{us:.2f},busbw={S*2*(a.P-1)/a.P/us/1e3:.1f}")
+    print(f"inproc{'-zc' if a.zero_copy else '-staged'}{'-graph' if a.graph else ''}-algo{a.algo},{a.P},{a.dims},{S},{us:.2f},busbw={S*2*(a.P-1)/a.P/us/1e3:.1f}")
 g.finalize()
