@@ -22,7 +22,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, q, env):
+def _rank_main(rank, world, port, q, env, dims):
     import torch.distributed as dist
     import oracle
     import synthetic_inputs as si
@@ -34,12 +34,12 @@ def _rank_main(rank, world, port, q, env):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     res = {}
     try:
-        comm = ddl.init([world], max_bytes=16 << 20)
+        comm = ddl.init(dims, max_bytes=16 << 20)
         for dtype, op in (("float32", "avg"), ("int32", "sum"), ("bfloat16", "sum")):
             kind = "fullrange" if dtype == "int32" else "normal"
             n = 50_003
             bufs = si.rank_buffers(dtype, kind, n, world)
-            want = oracle.allreduce(bufs, [world], dtype, op)[rank]
+            want = oracle.allreduce(bufs, dims, dtype, op)[rank]
             zc = comm.buffer(n, to_dev(bufs[0][:1], dtype).dtype)
             zc.copy_(to_dev(bufs[rank], dtype))
             st = to_dev(bufs[rank], dtype)
@@ -49,7 +49,7 @@ def _rank_main(rank, world, port, q, env):
             res[dtype] = (same_bits(to_host(zc), want), same_bits(to_host(st), want))
         # staged message larger than the workspace: reduced in pieces (ddl.Comm.all_reduce)
         big = si.rank_buffers("float32", "normal", 6_000_001, world, seed=5)
-        want = oracle.allreduce_sampled(big, [world], "float32", "avg", np.arange(0, 6_000_001, 997))
+        want = oracle.allreduce_sampled(big, dims, "float32", "avg", np.arange(0, 6_000_001, 997))
         tb = to_dev(big[rank], "float32")
         comm.all_reduce(tb, "avg")
         torch.cuda.synchronize()
@@ -62,7 +62,7 @@ def _rank_main(rank, world, port, q, env):
         view.copy_(to_dev(rb[rank], "float32"))
         comm.all_reduce(view, "avg")
         torch.cuda.synchronize()
-        res["registered"] = (same_bits(to_host(view), oracle.allreduce(rb, [world], "float32", "avg")[rank]),)
+        res["registered"] = (same_bits(to_host(view), oracle.allreduce(rb, dims, "float32", "avg")[rank]),)
         res["err"] = comm.async_error()
         comm.finalize()
     except Exception as e:  # report, don't hang the parent
@@ -71,20 +71,22 @@ def _rank_main(rank, world, port, q, env):
     dist.destroy_process_group()
 
 
-@pytest.mark.timeout(240)
-@pytest.mark.parametrize("env", [{}, {"DDL_TMA_MIN_SLICE_BYTES": "0"}], ids=["default", "tma"])
-def test_two_processes_ipc_one_gpu(env):
-    world = 2
+@pytest.mark.timeout(400)
+@pytest.mark.parametrize("world,dims,env", [(2, [2], {}), (2, [2], {"DDL_TMA_MIN_SLICE_BYTES": "0"}),
+                                            (4, [2, 2], {"DDL_TMA_MIN_SLICE_BYTES": "0"}),
+                                            (8, [4, 2], {})],
+                         ids=["2-default", "2-tma", "4-2x2-tma", "8-2x4"])
+def test_processes_ipc_one_gpu(world, dims, env):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, env)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, env, dims)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
     try:
         for _ in range(world):
-            r, res = q.get(timeout=200)
+            r, res = q.get(timeout=360)
             out[r] = res
     finally:
         for p in procs:
