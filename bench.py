@@ -261,17 +261,28 @@ def run_loopback(args):
     out_host = [torch.empty(s, dtype=torch.float32).pin_memory() for s in sizes]
     e2e_steps = max(3, min(args.steps, 10))
 
+    # pipelined like a user would: bucket b's H2D (copy stream) overlaps bucket b-1's
+    # all-reduce (compute stream) and bucket b-2's D2H (second copy stream)
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+
     def e2e_step():
         for b in range(nb):
-            for r in range(P):
-                bufs[b][r].copy_(pinned[b][r], non_blocking=True)
-            lb.all_reduce(bufs[b], "avg")
-            out_host[b].copy_(bufs[b][0], non_blocking=True)
+            with torch.cuda.stream(h2d_s):
+                for r in range(P):
+                    bufs[b][r].copy_(pinned[b][r], non_blocking=True)
+            stream.wait_stream(h2d_s)
+            lb.all_reduce(bufs[b], "avg", stream=stream)
+            d2h_s.wait_stream(stream)
+            with torch.cuda.stream(d2h_s):
+                out_host[b].copy_(bufs[b][0], non_blocking=True)
+        stream.wait_stream(d2h_s)
+        h2d_s.wait_stream(stream)   # the next step's H2D must not overwrite buffers still in use
 
     e2e_step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    h2d_s.wait_stream(stream)
     for _ in range(e2e_steps):
         e2e_step()
     e1.record(stream)
@@ -403,11 +414,19 @@ def run_multi(args):
     pinned = [torch.from_numpy(h).pin_memory() for h in host]
     outh = [torch.empty(s).pin_memory() for s in sizes]
 
-    def e2e_step():
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def e2e_step():   # pipelined: H2D of bucket b || all-reduce of b-1 || D2H of b-2
         for v, ph, oh in zip(views, pinned, outh):
-            v.copy_(ph, non_blocking=True)
-            comm.all_reduce(v, "avg")
-            oh.copy_(v, non_blocking=True)
+            with torch.cuda.stream(h2d_s):
+                v.copy_(ph, non_blocking=True)
+            stream.wait_stream(h2d_s)
+            comm.all_reduce(v, "avg", stream=stream)
+            d2h_s.wait_stream(stream)
+            with torch.cuda.stream(d2h_s):
+                oh.copy_(v, non_blocking=True)
+        stream.wait_stream(d2h_s)
+        h2d_s.wait_stream(stream)
     e2e_step()
     e2e_ms = timed(e2e_step, max(3, min(args.steps, 10)))
 
