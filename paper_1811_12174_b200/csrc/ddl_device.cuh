@@ -40,7 +40,7 @@ enum Mode : int {
 
 enum DType : int { kI32 = 0, kF32 = 1, kBF16 = 2 };
 enum Op : int { kSum = 0, kAvg = 1 };
-enum Err : int { kErrTimeout = 8 };
+enum Err : int { kErrTimeout = 8, kErrMismatch = 9 };
 
 struct KParams {
   Topo t;
@@ -65,6 +65,7 @@ struct KParams {
   int mode;
   uint64_t* trace;     // debug (DDL_TRACE=1): [P][cmax][kTraceEvents] globaltimer stamps, else null
   int stream_every;    // PATH 5: publish progress every k chunks (and at the phase end)
+  uint32_t sig;        // DDL_CHECK=1: signature of (count, dtype, op, algorithm); 0 = no check
 };
 constexpr int kTraceEvents = 40;
 
@@ -188,12 +189,19 @@ __device__ __forceinline__ uint32_t* flag_slot(const KParams& p, uint32_t* base,
 
 // Barrier `slot` of CTA blockIdx.x of rank `me` with `np` peers given by peer(l).
 // Returns false (after recording DDL_ERR_TIMEOUT) if a peer did not arrive in time.
+// DDL_CHECK: each rank's call signature, written into the peer's slot before the first
+// barrier's release (so the acquire of the epoch makes it visible).
+__device__ __forceinline__ uint32_t* sig_slot(const KParams& p, uint32_t* base, int cta, int src);
+
 template <typename PeerFn>
-__device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int np, uint32_t epoch, PeerFn peer) {
+__device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int np, uint32_t epoch, PeerFn peer,
+                                         bool check_sig = false) {
   __syncthreads();  // every thread's stores of the previous phase precede the release below
   int fail = 0;
   if (threadIdx.x < np) {
     const int m = peer(threadIdx.x);
+    const bool chk = check_sig && p.sig;
+    if (chk) *(volatile uint32_t*)sig_slot(p, p.flags[m], blockIdx.x, me) = p.sig;
     st_release(flag_slot(p, p.flags[m], slot, blockIdx.x, me), epoch, p.gpu_scope);
     const uint32_t* f = flag_slot(p, p.flags[me], slot, blockIdx.x, m);
     uint64_t t0 = 0;
@@ -203,11 +211,15 @@ __device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int
         const uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
         else if (now - t0 > p.timeout_ns) {
-          atomicExch(p.err, kErrTimeout);
+          atomicCAS(p.err, 0, kErrTimeout);
           fail = 1;
           break;
         }
       }
+    }
+    if (!fail && chk && *(volatile uint32_t*)sig_slot(p, p.flags[me], blockIdx.x, m) != p.sig) {
+      atomicCAS(p.err, 0, kErrMismatch);  // ranks disagree on (count, dtype, op, algorithm)
+      fail = 1;
     }
   }
   return __syncthreads_or(fail) == 0;
@@ -245,6 +257,16 @@ __device__ __forceinline__ uint32_t* steal_tick(const KParams& p, int r, int j) 
 }
 __device__ __forceinline__ uint32_t* steal_done(const KParams& p, int r, int j) {
   return steal_base(p, r) + 16 + (size_t)(kNumSlots + j) * p.cmax;
+}
+
+// after the steal counters: the PATH 5 progress words (kNumSlots x cmax u64), then the
+// DDL_CHECK signatures [cmax][kMaxRanks]
+__device__ __forceinline__ uint32_t* sig_slot(const KParams& p, uint32_t* base, int cta, int src) {
+  uint32_t* end = base + p.cmax + (size_t)kNumSlots * p.cmax * p.t.P + kRankStateWords + 16 +
+                  2 * (size_t)kNumSlots * p.cmax;
+  uint64_t* prog = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(end) + 7) & ~(uintptr_t)7);
+  uint32_t* sig = reinterpret_cast<uint32_t*>(prog + (size_t)kNumSlots * p.cmax);
+  return sig + (size_t)cta * kMaxRanks + src;
 }
 
 __device__ __forceinline__ uint32_t rank_epoch_begin(const KParams& p, int me) {
@@ -742,9 +764,10 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
 
   auto run = [&](const PhaseCtx& x, int j) {
     if constexpr (STREAM) {
-      if (x.kind == kPhRS || x.kind == kPhAG) {
-        const int first = (p.mode & kRS) ? 0 : L;
-        stream_phase<T>(p, me, x, pp, j, j > first, e);
+      // Streaming needs every source block's producing phase to publish progress; the
+      // copy-in of an allgather-only call does not, so that mode keeps its barriers.
+      if ((x.kind == kPhRS || x.kind == kPhAG) && (p.mode & kRS)) {
+        stream_phase<T>(p, me, x, pp, j, j > 0, e);
         return;
       }
     }
@@ -781,7 +804,7 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
     for (int j = 0; j < L; ++j) {
       if (!settle(j)) return;
       if (!(j == 0 && implied_start) && !(STREAM && j > 0) &&
-          !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j)))
+          !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j), j == 0))
         return;
       trace_ev(p, me, 2 + 2 * j);
       prev = phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1);
@@ -794,7 +817,8 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
     for (int jj = 0; jj < L; ++jj) {
       const int j = L + jj;
       if (!settle(j)) return;
-      if (!(STREAM && (jj > 0 || (p.mode & kRS))) && !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j)))
+      if (!(STREAM && (p.mode & kRS)) &&
+          !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j), jj == 0 && !(p.mode & kRS)))
         return;
       trace_ev(p, me, 2 + 2 * j);
       prev = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false);
@@ -881,7 +905,7 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_c
     }
   }
   // loopback without copy-in: inputs are ready at launch (see ddl_hier_kernel)
-  if (!(p.loopback && !(p.mode & kCinAll)) && !dbarrier(p, me, 0, P - 1, e, all)) return;
+  if (!(p.loopback && !(p.mode & kCinAll)) && !dbarrier(p, me, 0, P - 1, e, all, true)) return;
 
   A res[R][W];
 #pragma unroll

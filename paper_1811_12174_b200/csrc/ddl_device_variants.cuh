@@ -70,7 +70,7 @@ __device__ __forceinline__ bool own_slice_done(const KParams& p, int me, const P
         const uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
         else if (now - t0 > p.timeout_ns) {
-          atomicExch(p.err, kErrTimeout);
+          atomicCAS(p.err, 0, kErrTimeout);
           s_fail = 1;
           break;
         }
@@ -398,7 +398,7 @@ __device__ void stream_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& 
           const uint64_t now = globaltimer();
           if (t0 == 0) t0 = now;
           else if (now - t0 > p.timeout_ns) {
-            atomicExch(p.err, kErrTimeout);
+            atomicCAS(p.err, 0, kErrTimeout);
             return false;
           }
         }
@@ -579,7 +579,7 @@ __device__ __forceinline__ bool rank_wait(const KParams& p, int me, int slot, ui
         const uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
         else if (now - t0 > p.timeout_ns) {
-          atomicExch(p.err, kErrTimeout);
+          atomicCAS(p.err, 0, kErrTimeout);
           fail = 1;
           break;
         }

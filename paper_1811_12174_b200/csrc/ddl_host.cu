@@ -121,6 +121,7 @@ struct ddl_comm {
   int skip_rank = -1;
   bool use_tma = true;
   bool use_steal = false;  // DDL_STEAL=1: per-CTA slices + work stealing (PATH 4)
+  bool check = false;       // DDL_CHECK=1: ranks compare (count, dtype, op, algorithm) at the first barrier
   bool use_stream = false;  // DDL_STREAM=1: no inner phase barriers, per-chunk progress (PATH 5)
   bool use_dyn = false;     // DDL_DYN=1: rank-level barriers + dynamic chunks (measured slower)
   int gpu_share = 1;        // ranks sharing this GPU (loopback: P; in-process test groups: P)
@@ -179,6 +180,7 @@ void apply_env(ddl_comm* c) {
   c->use_dyn = env_size("DDL_DYN", 0) != 0;
   c->use_steal = env_size("DDL_STEAL", 0) != 0;
   c->use_stream = env_size("DDL_STREAM", 0) != 0;
+  c->check = env_size("DDL_CHECK", 0) != 0;
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
@@ -200,7 +202,8 @@ ddl_result_t common_init(ddl_comm* c, int nranks, const int* dims, int ndims, in
   c->cmax = c->num_sms * 4;
   const size_t words = (size_t)c->cmax * (1 + (size_t)kNumSlots * nranks) + kRankStateWords +
                        16 + 2 * (size_t)kNumSlots * c->cmax +  // + steal counters
-                       2 + 2 * (size_t)kNumSlots * c->cmax;    // + streaming progress words
+                       2 + 2 * (size_t)kNumSlots * c->cmax +   // + streaming progress words
+                       (size_t)c->cmax * kMaxRanks;             // + DDL_CHECK signatures
   c->flags_bytes = (words * 4 + 65535) / 65536 * 65536;
   apply_env(c);
   if (env_size("DDL_TRACE", 0)) {
@@ -337,7 +340,16 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
   return p;
 }
 
-ddl_result_t launch(const ddl_comm* c, const KParams& p, const Plan& pl, ddl_dtype_t dt, void* stream) {
+ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dtype_t dt, void* stream) {
+  KParams p = p0;
+  if (c->check && !c->loopback) {  // FNV-1a over what every rank must agree on
+    uint32_t h = 2166136261u;
+    const uint64_t vals[] = {p.n, (uint64_t)dt, (uint64_t)p.op, (uint64_t)p.mode, (uint64_t)pl.oneshot,
+                             (uint64_t)pl.path, (uint64_t)pl.nctas, p.q};
+    for (uint64_t v : vals)
+      for (int b = 0; b < 8; ++b) h = (h ^ (uint32_t)((v >> (8 * b)) & 0xFF)) * 16777619u;
+    p.sig = h | 1u;
+  }
   const void* fn = pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive, pl.r) : hier_fn_dt(dt, pl.path);
   if (!fn) return DDL_ERR_UNSUPPORTED;
   const size_t smem = pl.oneshot ? 0 : hier_smem(pl.path);

@@ -56,7 +56,8 @@ def group(P, dims, env=None):
 # every hierarchical kernel variant of the multi-process launch path
 VARIANTS = {"default": None, "tma": {"DDL_TMA_MIN_SLICE_BYTES": "0"},
             "stream": {"DDL_STREAM": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"},
-            "steal": {"DDL_STEAL": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"}}
+            "steal": {"DDL_STEAL": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"},
+            "check": {"DDL_CHECK": "1"}}
 
 
 CASES = [(2, [2]), (4, [2, 2]), (4, [4]), (8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (6, [3, 2])]
@@ -191,3 +192,24 @@ def test_zero_copy_reduce_scatter_allgather(variant):
         torch.cuda.synchronize()
         for r in range(P):
             assert same_bits(to_host(target[r]), wantg[r]), ("ag", r)
+
+
+def test_collective_mismatch_detected():
+    """DDL_CHECK=1: ranks calling with different counts get DDL_ERR_MISMATCH (sticky),
+    not silent garbage; agreeing calls pass (the 'check' variant above)."""
+    os.environ["DDL_TIMEOUT_MS"] = "300"
+    try:
+        g = group(2, [2], {"DDL_CHECK": "1", "DDL_TIMEOUT_MS": "300"})
+    finally:
+        os.environ["DDL_TIMEOUT_MS"] = "5000"
+    L = ddl.lib()
+    ts = [torch.ones(4096, device="cuda") for _ in range(2)]
+    counts = [4096, 2048]
+    cur = torch.cuda.current_stream()
+    for r in range(2):
+        g.streams[r].wait_stream(cur)
+    for r in range(2):
+        assert L.ddl_allreduce(g.hs[r], ts[r].data_ptr(), counts[r], ddl.FLOAT32, ddl.SUM,
+                               g.streams[r].cuda_stream) == ddl.SUCCESS
+    torch.cuda.synchronize()
+    assert g.async_error() == ddl.ERR_MISMATCH
