@@ -30,7 +30,12 @@
  *     NULL = legacy default stream).  Argument errors return synchronously and enqueue
  *     nothing.  Device-side errors (a peer that never arrives: DDL_ERR_TIMEOUT) are
  *     sticky and read with ddl_async_error().
- *   - Every rank calls the same sequence of collectives with equal (count, dtype, op).
+ *   - Every rank calls the same sequence of collectives with equal (count, dtype, op)
+ *     (DDL_CHECK=1 verifies it on the device: DDL_ERR_MISMATCH).  Calls on one
+ *     communicator must be ordered (one stream, or externally serialised): the device
+ *     barriers of consecutive calls are told apart by a per-rank call counter.
+ *   - Calls are CUDA-graph capturable: all per-call state (the call counter, the flags)
+ *     lives in device memory.
  *   - The caller owns buffers, streams and the comm handle; the library owns its
  *     workspace, flags and IPC mappings and releases them in ddl_finalize().  No C++
  *     exception crosses the ABI and the library never aborts the process.

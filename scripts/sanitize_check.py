@@ -9,8 +9,14 @@ def check(bufs, want):
     torch.cuda.synchronize()
     assert all(bool((b == want).all()) for b in bufs)
 
-for P, dims in ((4, [2, 2]), (8, [4, 2]), (3, [3])):
+import os
+runs = [((4, [2, 2]), None), ((8, [4, 2]), None), ((3, [3]), None),
+        ((4, [2, 2]), "DDL_TMA_MIN_SLICE_BYTES"), ((8, [4, 2]), "DDL_TMA_MIN_SLICE_BYTES")]
+for (P, dims), force in runs:
+    if force:
+        os.environ[force] = "0"          # TMA-staged path even for these tiny slices
     lb = ddl.Loopback(P, dims)
+    os.environ.pop("DDL_TMA_MIN_SLICE_BYTES", None)
     for algo in (ddl.ALGO_HIER, ddl.ALGO_ONESHOT):
         lb.set_algo(algo, 1 << 30)
         for n in (1, 1003, 70_001):
@@ -31,7 +37,9 @@ for P, dims in ((4, [2, 2]), (8, [4, 2]), (3, [3])):
         want = torch.arange(1, P + 1, device="cuda", dtype=torch.float32).repeat_interleave(recv)
         assert all(torch.equal(x, want) for x in g)
     lb.finalize()
+os.environ["DDL_TMA_MIN_SLICE_BYTES"] = "0"
 g = ddl.InProcessGroup(2, [2], max_bytes=1 << 20)
+os.environ.pop("DDL_TMA_MIN_SLICE_BYTES", None)
 for n in (5, 4099):
     zc = [g.buffer(r, n, torch.float32) for r in range(2)]
     for r in range(2):
