@@ -191,6 +191,13 @@ def check_sampled(bufs, dev, dims, dtype, op):
     for r, t in enumerate(dev):
         got = to_host(t[ti])
         assert same_bits(got, want), (dims, r, first_diff(got, want))
+    if dtype == "float32":       # north_star tolerance vs an fp64 naive sum (ledger 8: |y - s| / sum|x|)
+        s64, a64 = oracle.exact_sum_f64([np.asarray(b)[idx] for b in bufs], "float32")
+        P = len(bufs)
+        ref = s64 / P if op == "avg" else s64
+        mag = a64 / P if op == "avg" else a64
+        y = to_host(dev[0][ti]).astype(np.float64)
+        assert np.max(np.abs(y - ref) / np.maximum(mag, 1e-300)) <= 1e-6
     for t in dev[1:]:            # all ranks identical, every element
         assert torch.equal(t.view(torch.int16) if t.dtype == torch.bfloat16 else t,
                            dev[0].view(torch.int16) if t.dtype == torch.bfloat16 else dev[0])
