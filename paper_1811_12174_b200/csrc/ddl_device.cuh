@@ -36,6 +36,7 @@ enum Mode : int {
   kRS = 4,
   kAG = 8,
   kCoutAll = 16,  // copy work[me] -> cout[me] (all blocks) after the AG phases
+  kScratch = 32,  // one-shot, multi-process: inputs published through double-buffered scratch
 };
 
 enum DType : int { kI32 = 0, kF32 = 1, kBF16 = 2 };
@@ -66,6 +67,8 @@ struct KParams {
   uint64_t* trace;     // debug (DDL_TRACE=1): [P][cmax][kTraceEvents] globaltimer stamps, else null
   int stream_every;    // PATH 5: publish progress every k chunks (and at the phase end)
   uint32_t sig;        // DDL_CHECK=1: signature of (count, dtype, op, algorithm); 0 = no check
+  char* scratch[kMaxRanks];  // kScratch: each rank's one-shot scratch (two halves, by call parity)
+  uint64_t scratch_half;     // bytes per half
 };
 constexpr int kTraceEvents = 40;
 
@@ -893,9 +896,16 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_c
   const uint64_t hi = lo + p.slice < p.n ? lo + p.slice : p.n;
   auto all = [me](int l) { return all_peer(me, l); };
 
-  if (p.mode & kCinAll) {  // staged: publish this CTA's slice of my input
+  // kScratch (multi-process): my input goes to scratch half (e & 1); peers read only the
+  // scratch, never my buffer, so the result can be written without a second barrier.  A
+  // half is reused two calls later, when every peer has provably finished this call (it
+  // signalled the call in between).
+  const char* src_of[kMaxRanks];
+  for (int r = 0; r < P; ++r)
+    src_of[r] = (p.mode & kScratch) ? p.scratch[r] + (e & 1u) * p.scratch_half : static_cast<const char*>(p.in[r]);
+  if (p.mode & (kCinAll | kScratch)) {  // publish this CTA's slice of my input
     const char* s = static_cast<const char*>(p.cin[me]);
-    char* w = static_cast<char*>(p.work[me]);
+    char* w = (p.mode & kScratch) ? const_cast<char*>(src_of[me]) : static_cast<char*>(p.work[me]);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const uint64_t eo = lo + ((uint64_t)i * blockDim.x + threadIdx.x) * W;
@@ -920,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_c
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
           if (r0 + k >= P) break;
-          raw[k] = ld_vec(static_cast<const char*>(p.in[r0 + k]) + eoff * sizeof(T));
+          raw[k] = ld_vec(src_of[r0 + k] + eoff * sizeof(T));
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -935,14 +945,14 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_c
         A lvl1[K][1];
         A r1[1];
         for (int r = 0; r < P; ++r) {
-          A x[1] = {Tr<T>::to(ld_elem<T>(static_cast<const char*>(p.in[r]) + (eoff + k) * sizeof(T)))};
+          A x[1] = {Tr<T>::to(ld_elem<T>(src_of[r] + (eoff + k) * sizeof(T)))};
           nested_feed<T, K, 1>(p, gl, Gl, r, lvl1, x, r1);
         }
         res[i][k] = r1[0];
       }
     }
   }
-  if (!dbarrier(p, me, 1, P - 1, e, all)) return;
+  if (!(p.mode & kScratch) && !dbarrier(p, me, 1, P - 1, e, all)) return;
   char* o = static_cast<char*>(p.out[me]);
 #pragma unroll
   for (int i = 0; i < R; ++i) {

@@ -55,7 +55,7 @@ struct Handle {  // exported per rank, all-gathered by the caller
   int32_t dims[kMaxDims];
   int32_t cmax;
   int32_t pad;
-  uint64_t flags_bytes, max_bytes, alloc_bytes;
+  uint64_t flags_bytes, max_bytes, alloc_bytes, scratch_half;
   char pci[32];
   cudaIpcMemHandle_t ipc;
 };
@@ -152,6 +152,8 @@ struct ddl_comm {
   };
   std::vector<Mapping> maps;
   char* stage_of(int r) const { return (r == rank ? alloc : peer_base[r]) + flags_bytes + max_bytes; }
+  size_t scratch_half = 0;  // one-shot scratch: two halves after the staging area
+  char* scratch_of(int r) const { return stage_of(r) + max_bytes; }
 };
 
 namespace {
@@ -316,6 +318,7 @@ bool plan_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
 
 bool use_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
   if (c->P < 2 || c->algo == DDL_ALGO_HIER) return false;
+  if (!c->loopback && n * (uint64_t)elem_size(dt) > c->scratch_half) return false;  // scratch-bound
   if (c->algo == DDL_ALGO_AUTO && n * (uint64_t)elem_size(dt) > c->oneshot_max) return false;
   return plan_oneshot(c, n, dt, pl);
 }
@@ -514,7 +517,8 @@ ddl_result_t ddl_init(ddl_comm_t* comm, int rank, int nranks, const int* dims, i
   }
   c->rank = rank;
   c->max_bytes = (max_bytes + 4095) / 4096 * 4096;
-  c->alloc_bytes = c->flags_bytes + 2 * c->max_bytes;
+  c->scratch_half = ((c->oneshot_max > (512u << 10) ? c->oneshot_max : (512u << 10)) + 4095) / 4096 * 4096;
+  c->alloc_bytes = c->flags_bytes + 2 * c->max_bytes + 2 * c->scratch_half;
   cudaError_t e = cudaMalloc(&c->alloc, c->alloc_bytes);
   if (e == cudaSuccess) e = cudaMemset(c->alloc, 0, c->flags_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int));
@@ -545,6 +549,7 @@ ddl_result_t ddl_export_handle(ddl_comm_t c, void* out) {
   h.cmax = c->cmax;
   h.flags_bytes = c->flags_bytes;
   h.max_bytes = c->max_bytes;
+  h.scratch_half = c->scratch_half;
   h.alloc_bytes = c->alloc_bytes;
   DDL_CUDA(cudaSetDevice(c->device));
   DDL_CUDA(cudaDeviceGetPCIBusId(h.pci, sizeof(h.pci), c->device));
@@ -562,7 +567,7 @@ ddl_result_t ddl_connect(ddl_comm_t c, const void* all_handles) {
     const Handle& h = hs[m];
     if (h.magic != kMagic || h.rank != m) return DDL_ERR_INVALID_ARGUMENT;
     if (h.nranks != c->P || h.ndims != c->ndims || h.cmax != c->cmax || h.flags_bytes != c->flags_bytes ||
-        h.max_bytes != c->max_bytes)
+        h.max_bytes != c->max_bytes || h.scratch_half != c->scratch_half)
       return DDL_ERR_MISMATCH;
     for (int d = 0; d < c->ndims; ++d)
       if (h.dims[d] != c->dims[d]) return DDL_ERR_MISMATCH;
@@ -625,9 +630,12 @@ ddl_result_t ddl_allreduce(ddl_comm_t c, void* buf, size_t count, ddl_dtype_t dt
     p.out[m] = base;
   }
   if (one) {
-    p.mode = zero_copy ? 0 : kCinAll;
+    // one barrier: inputs are published through the double-buffered scratch
+    p.mode = kScratch;
     p.cin[c->rank] = buf;
     p.out[c->rank] = buf;
+    for (int m = 0; m < c->P; ++m) p.scratch[m] = c->scratch_of(m);
+    p.scratch_half = c->scratch_half;
   } else {
     p.mode = kRS | kAG | (zero_copy ? 0 : (kCinAll | kCoutAll));
     p.cin[c->rank] = buf;
@@ -758,7 +766,7 @@ ddl_result_t ddl_debug_connect_local(ddl_comm_t* comms, int nranks) {
     const ddl_comm* c = comms[r];
     if (!c || c->loopback || c->rank != r || c->P != nranks) return DDL_ERR_INVALID_ARGUMENT;
     if (c->ndims != comms[0]->ndims || c->max_bytes != comms[0]->max_bytes || c->cmax != comms[0]->cmax ||
-        c->device != comms[0]->device)
+        c->device != comms[0]->device || c->scratch_half != comms[0]->scratch_half)
       return DDL_ERR_MISMATCH;
     for (int d = 0; d < c->ndims; ++d)
       if (c->dims[d] != comms[0]->dims[d]) return DDL_ERR_MISMATCH;
