@@ -35,7 +35,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
 
 import synthetic_inputs as si  # noqa: E402
 

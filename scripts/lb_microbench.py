@@ -1,7 +1,7 @@
 """Loopback micro-benchmark: time one all-reduce (P virtual ranks on one GPU) per size.
 python scripts/lb_microbench.py --P 8 --dims 2x4 --sizes 31502336 --dtype float32 --op avg
 Prints one CSV row per size: lib,P,dims,dtype,bytes,us,algbw_GBs,busbw_GBs,hbm_alg_GBs."""
-import argparse, math, os, sys
+import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1811_12174_b200 import ddl

@@ -6,14 +6,12 @@
 * argument validation returns the documented error codes without touching a GPU;
 * the multi-process bootstrap (handle exchange) works at world_size 2 over gloo.
 """
-import math
 import os
 import re
 import socket
 
 import numpy as np
 import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 

@@ -4,7 +4,6 @@ P:L56-60) in real processes on one GPU: bit-exact vs the oracle with dims = inne
 import os
 import socket
 
-import numpy as np
 import pytest
 import torch
 import torch.multiprocessing as mp

@@ -7,7 +7,6 @@ fixed reduction order; all NaNs compare equal.  At full BASELINE sizes the oracl
 sampled elements (oracle.allreduce_sampled), and properties that hold at any size (all
 ranks identical, closed forms) cover the rest.
 """
-import math
 
 import numpy as np
 import pytest

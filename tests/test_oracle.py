@@ -8,7 +8,6 @@ A plausible oracle mistake -- a dropped term, a wrong group member or coordinate
 transposed fold order, a missing phase-boundary rounding, a misplaced avg multiply, a
 wrong block range -- fails at least one of these.  CPU only (no GPU marker).
 """
-import itertools
 import json
 import math
 import os
@@ -292,7 +291,6 @@ def test_bf16_round_matches_libraries():
                          np.finfo(np.float32).max, -np.finfo(np.float32).max, 3.3895e38, 3.4e38,
                          np.inf, -np.inf, 1e-40, -1e-40, 2**-133, 1.17549435e-38, 65504.0,
                          np.float32(1.00390625), 255.5, 256.5], dtype=np.float32)
-    r = oracle.ddl_oracle.rng if False else None  # noqa: F841  (no oracle RNG; inputs below)
     rnd = np.random.Generator(np.random.PCG64(7))
     bits = rnd.integers(0, 1 << 32, size=200000, dtype=np.uint32)
     bits = bits[((bits >> 23) & 0xFF) != 0xFF]                       # finite patterns
