@@ -67,3 +67,23 @@ def test_loopback_rejects_multiprocess_calls():
     t = torch.ones(64, device="cuda")
     assert L.ddl_allreduce(lb.h, t.data_ptr(), 64, ddl.FLOAT32, ddl.SUM, None) == ddl.ERR_INVALID_ARGUMENT
     lb.finalize()
+
+
+def test_plain_c_program_on_gpu(tmp_path):
+    """examples/loopback_allreduce.c: the C ABI driven from C alone (cudaMalloc'd buffers,
+    no Python/torch on the data path) reduces correctly on the GPU."""
+    import os
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1811_12174_b200")
+    exe = tmp_path / "lb"
+    subprocess.run(["gcc", "-std=c99", "-O2", "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+                    os.path.join(root, "examples", "loopback_allreduce.c"), "-L", libdir, "-lddl",
+                    "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{libdir}:/usr/local/cuda/lib64",
+                    "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "loopback_allreduce ok" in r.stdout
