@@ -318,9 +318,11 @@ def run_loopback(args):
                    "bucket_us": [round(u, 1) for u in bucket_us]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
-                     "traffic": profiled_traffic("resnet50-grad-set 8 virtual ranks dims 2x4 avg")
-                     if dims == [4, 2] else None,
-                     "traffic_unit": "DRAM bytes per step (all 5 launches), ncu --set full, profiles/traffic.json",
+                     "traffic": (tr // nb if (tr := profiled_traffic("resnet50-grad-set 8 virtual ranks dims 2x4 avg"))
+                                 and dims == [4, 2] else None),
+                     "traffic_unit": "DRAM bytes per launch (mean of the 5 bucket launches of one step), "
+                                     "ncu --set full, profiles/traffic.json",
+                     "algorithmic_bytes_per_launch": algo_bytes // args.steps // nb,
                      "peak_source": peak_src,
                      "kernel": "ddl_hier_kernel<float,true> (loopback, all 8 virtual ranks)",
                      "algorithmic_bytes_per_step": algo_bytes // args.steps,
