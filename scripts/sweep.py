@@ -90,8 +90,12 @@ def loopback(args, out):
 def multi(args, out):
     import torch.distributed as dist
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    same_gpu = os.environ.get("DDL_BENCH_SAME_GPU") == "1"   # functional check on one GPU (no NCCL rows)
+    torch.cuda.set_device(0 if same_gpu else local)
+    if same_gpu:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comms = {}
     for P, spec, dtype, op, S in rows_for(args.config):
         if P not in (None, world):
@@ -114,24 +118,28 @@ def multi(args, out):
         iters = max(3, min(200, int(2e9 // max(S, 1))))
         dist.barrier()
         us = time_graph(lambda: comm.all_reduce(t, op), iters)
-        nt = torch.full((n,), rank + 1, dtype=TD[dtype], device="cuda")
-        nccl_op = dist.ReduceOp.AVG if op == "avg" else dist.ReduceOp.SUM
-        for _ in range(3):
-            dist.all_reduce(nt, op=nccl_op)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dist.barrier()
-        e0.record()
-        for _ in range(iters):
-            dist.all_reduce(nt, op=nccl_op)
-        e1.record()
-        torch.cuda.synchronize()
-        nus = e0.elapsed_time(e1) * 1e3 / iters
-        m = torch.tensor([us, nus], device="cuda")
+        nus = float("nan")
+        if not same_gpu:
+            nt = torch.full((n,), rank + 1, dtype=TD[dtype], device="cuda")
+            nccl_op = dist.ReduceOp.AVG if op == "avg" else dist.ReduceOp.SUM
+            for _ in range(3):
+                dist.all_reduce(nt, op=nccl_op)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dist.barrier()
+            e0.record()
+            for _ in range(iters):
+                dist.all_reduce(nt, op=nccl_op)
+            e1.record()
+            torch.cuda.synchronize()
+            nus = e0.elapsed_time(e1) * 1e3 / iters
+        m = torch.tensor([us, nus], device="cpu" if same_gpu else "cuda")
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         us, nus = m.tolist()
         if rank == 0:
             for impl, tt in (("ddl", us), ("nccl", nus)):
+                if tt != tt:   # NaN: not measured
+                    continue
                 bus = S * 2 * (world - 1) / world / tt / 1e3
                 print(",".join(map(str, [impl, world, spec, dtype, op, S, f"{tt:.2f}", f"{S / tt / 1e3:.2f}",
                                          f"{bus:.2f}", f"{bus / 900 * 100:.1f}", "nvlink900"])), file=out, flush=True)
