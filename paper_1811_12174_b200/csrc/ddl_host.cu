@@ -39,6 +39,24 @@ ddl_result_t cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
   } while (0)
 
+// Switches to the communicator's device for the duration of an API call and restores the
+// caller's current device afterwards (the ABI never leaves the caller's device changed).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+#define DDL_ON_DEVICE(dev)                                              \
+  DeviceGuard dg_(dev);                                                 \
+  if (dg_.err != cudaSuccess) return cuda_fail(dg_.err, "cudaSetDevice")
+
 size_t env_size(const char* name, size_t dflt) {
   const char* v = std::getenv(name);
   if (!v || !*v) return dflt;
@@ -508,6 +526,7 @@ ddl_result_t ddl_init(ddl_comm_t* comm, int rank, int nranks, const int* dims, i
                       size_t max_bytes) {
   if (!comm || rank < 0 || rank >= nranks) return DDL_ERR_INVALID_ARGUMENT;
   *comm = nullptr;
+  DeviceGuard guard(cuda_device < 0 ? 0 : cuda_device);
   ddl_comm* c = new (std::nothrow) ddl_comm();
   if (!c) return DDL_ERR_CUDA;
   ddl_result_t r = common_init(c, nranks, dims, ndims, cuda_device);
@@ -551,7 +570,7 @@ ddl_result_t ddl_export_handle(ddl_comm_t c, void* out) {
   h.max_bytes = c->max_bytes;
   h.scratch_half = c->scratch_half;
   h.alloc_bytes = c->alloc_bytes;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   DDL_CUDA(cudaDeviceGetPCIBusId(h.pci, sizeof(h.pci), c->device));
   DDL_CUDA(cudaIpcGetMemHandle(&h.ipc, c->alloc));
   std::memcpy(out, &h, sizeof(h));
@@ -561,7 +580,7 @@ ddl_result_t ddl_export_handle(ddl_comm_t c, void* out) {
 ddl_result_t ddl_connect(ddl_comm_t c, const void* all_handles) {
   if (!c || !all_handles || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
   if (c->connected) return DDL_SUCCESS;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   const Handle* hs = static_cast<const Handle*>(all_handles);
   for (int m = 0; m < c->P; ++m) {
     const Handle& h = hs[m];
@@ -615,7 +634,7 @@ ddl_result_t ddl_allreduce(ddl_comm_t c, void* buf, size_t count, ddl_dtype_t dt
   }
   const bool zero_copy = in_sym || reg;
   if (!zero_copy && bytes > c->max_bytes) return DDL_ERR_TOO_LARGE;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   KParams p = base_params(c, count, op);
   Plan pl;
   const bool one = use_oneshot(c, count, dt, &pl);
@@ -655,7 +674,7 @@ ddl_result_t ddl_reduce_scatter(ddl_comm_t c, const void* sendbuf, void* recvbuf
   if (c->P == 1) return local_copy(sendbuf, recvbuf, recvcount, dt, stream);
   const size_t n = recvcount * (size_t)c->P;
   if (n * w > c->max_bytes) return DDL_ERR_TOO_LARGE;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   const bool vec = (recvcount * w) % 16 == 0;
   Plan pl = plan_hier(c, n, recvcount, dt, vec);
   KParams p = base_params(c, n, op);
@@ -690,7 +709,7 @@ ddl_result_t ddl_allgather(ddl_comm_t c, const void* sendbuf, void* recvbuf, siz
   const size_t n = sendcount * (size_t)c->P;
   const char* chk[kMaxRanks];
   if (n * w > c->max_bytes && !zero_copy_peers(c, recvbuf, n * w, chk)) return DDL_ERR_TOO_LARGE;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   const bool vec = (sendcount * w) % 16 == 0;
   Plan pl = plan_hier(c, n, sendcount, dt, vec);
   KParams p = base_params(c, n, DDL_SUM);
@@ -711,7 +730,7 @@ ddl_result_t ddl_allgather(ddl_comm_t c, const void* sendbuf, void* recvbuf, siz
 
 ddl_result_t ddl_async_error(ddl_comm_t c) {
   if (!c) return DDL_ERR_INVALID_ARGUMENT;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   DDL_CUDA(cudaDeviceSynchronize());
   int v = 0;
   DDL_CUDA(cudaMemcpy(&v, c->err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -784,7 +803,7 @@ size_t ddl_reg_handle_size(void) { return sizeof(RegHandle); }
 
 ddl_result_t ddl_register_export(ddl_comm_t c, void* ptr, size_t bytes, void* out) {
   if (!c || !ptr || !out || c->loopback || bytes == 0 || !aligned16(ptr)) return DDL_ERR_INVALID_ARGUMENT;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   char* base = nullptr;
   DDL_CUDA(alloc_base(ptr, &base));
   RegHandle h;
@@ -813,7 +832,7 @@ ddl_result_t ddl_register_connect(ddl_comm_t c, void* ptr, const void* all_handl
     if (hs[m].bytes != hs[c->rank].bytes) return DDL_ERR_MISMATCH;
   const int k = free_reg(c);
   if (k < 0) return DDL_ERR_UNSUPPORTED;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   ddl_comm::Reg g;
   g.local = static_cast<char*>(ptr);
   g.bytes = hs[c->rank].bytes;
@@ -860,7 +879,7 @@ static void release_reg(ddl_comm* c, int k) {
 
 ddl_result_t ddl_deregister(ddl_comm_t c, int reg_id) {
   if (!c || reg_id < 0 || reg_id >= ddl_comm::kMaxRegs || !c->regs[reg_id].used) return DDL_ERR_INVALID_ARGUMENT;
-  cudaSetDevice(c->device);
+  DeviceGuard dg_(c->device);
   cudaDeviceSynchronize();
   release_reg(c, reg_id);
   return DDL_SUCCESS;
@@ -890,7 +909,7 @@ ddl_result_t ddl_debug_register_local(ddl_comm_t* comms, void* const* ptrs, size
 
 ddl_result_t ddl_finalize(ddl_comm_t c) {
   if (!c) return DDL_SUCCESS;
-  cudaSetDevice(c->device);
+  DeviceGuard dg_(c->device);
   cudaDeviceSynchronize();
   for (int k = 0; k < ddl_comm::kMaxRegs; ++k)
     if (c->regs[k].used) release_reg(c, k);
@@ -909,6 +928,7 @@ ddl_result_t ddl_finalize(ddl_comm_t c) {
 ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, int ndims, int cuda_device) {
   if (!comm) return DDL_ERR_INVALID_ARGUMENT;
   *comm = nullptr;
+  DeviceGuard guard(cuda_device < 0 ? 0 : cuda_device);
   ddl_comm* c = new (std::nothrow) ddl_comm();
   if (!c) return DDL_ERR_CUDA;
   c->loopback = true;
@@ -948,7 +968,7 @@ ddl_result_t ddl_group_allreduce(ddl_comm_t c, void* const* bufs, size_t count, 
   if (!c->loopback) return DDL_ERR_INVALID_ARGUMENT;
   if (count == 0 || c->P == 1) return DDL_SUCCESS;
   if ((r = check_ptrs(c, bufs)) != DDL_SUCCESS) return r;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   KParams p = base_params(c, count, op);
   Plan pl;
   const bool one = use_oneshot(c, count, dt, &pl);
@@ -975,7 +995,7 @@ ddl_result_t ddl_group_reduce_scatter(ddl_comm_t c, const void* const* sendbufs,
   if (c->P == 1) return local_copy(sendbufs[0], recvbufs[0], recvcount, dt, stream);
   const int w = elem_size(dt);
   const size_t n = recvcount * (size_t)c->P;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   const size_t need = (n * w + 255) / 256 * 256;
   if (need > c->lb_ws_bytes) {
     DDL_CUDA(cudaDeviceSynchronize());
@@ -1010,7 +1030,7 @@ ddl_result_t ddl_group_allgather(ddl_comm_t c, const void* const* sendbufs, void
   if (c->P == 1) return local_copy(sendbufs[0], recvbufs[0], sendcount, dt, stream);
   const int w = elem_size(dt);
   const size_t n = sendcount * (size_t)c->P;
-  DDL_CUDA(cudaSetDevice(c->device));
+  DDL_ON_DEVICE(c->device);
   const bool vec = (sendcount * w) % 16 == 0;
   Plan pl = plan_hier(c, n, sendcount, dt, vec);
   KParams p = base_params(c, n, DDL_SUM);
