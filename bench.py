@@ -324,7 +324,7 @@ def run_loopback(args):
                                      "ncu --set full, profiles/traffic.json",
                      "algorithmic_bytes_per_launch": algo_bytes // args.steps // nb,
                      "peak_source": peak_src,
-                     "kernel": "ddl_hier_kernel<float,true> (loopback, all 8 virtual ranks)",
+                     "kernel": "ddl_hier_kernel<float,2> (TMA-staged; loopback, all 8 virtual ranks in one launch)",
                      "algorithmic_bytes_per_step": algo_bytes // args.steps,
                      "kernel_ms_per_step": kern_ms / args.steps},
         "e2e": {"value": S_total * 2 * (P - 1) / P / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
