@@ -320,9 +320,28 @@ class Comm:
             self.h = None
 
 
+def auto_dims(world: int, local_world: int | None = None) -> list[int]:
+    """Topology-aware factorisation (the role of ddlrun's topology config files):
+    ranks of one node share NVSwitch, where every pair has the same bandwidth, so one flat
+    dimension (fewest phases and barriers) is best inside a node -- measured in loopback
+    (profiles/r01_loopback_sweep.csv: [8] beats 2x4 and 2x2x2 at every size).  Across nodes
+    the node is the outer dimension (see multinode.TwoLevelComm for the off-node fabric)."""
+    import os
+    if local_world is None:
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    local_world = max(1, min(local_world, world))
+    if world % local_world:
+        raise DDLError(ERR_BAD_DIMS, f"{world} ranks do not split into nodes of {local_world}")
+    nodes = world // local_world
+    return [local_world] if nodes == 1 else [local_world, nodes]
+
+
 def init(dims=None, group=None, max_bytes: int = 256 << 20) -> Comm:
     """``ddl.init(dims)``: the analogue of the paper's ``import ddl`` + ``ddlrun`` setup
-     under torchrun."""
+     under torchrun.  ``dims="auto"`` picks :func:`auto_dims`."""
+    if isinstance(dims, str) and dims == "auto":
+        import torch.distributed as dist
+        dims = auto_dims(dist.get_world_size(group))
     return Comm(dims, group, max_bytes)
 
 

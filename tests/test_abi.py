@@ -208,3 +208,11 @@ def test_plain_c_client(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert "c_abi_smoke ok" in r.stdout
+
+
+def test_auto_dims():
+    assert ddl.auto_dims(8, 8) == [8]            # one NVSwitch node: flat
+    assert ddl.auto_dims(8, 4) == [4, 2]         # "2x4": 2 nodes x 4 GPUs
+    assert ddl.auto_dims(16, 8) == [8, 2]
+    with pytest.raises(ddl.DDLError):
+        ddl.auto_dims(8, 3)
