@@ -1019,4 +1019,76 @@ __global__ void __launch_bounds__(kThreads, 2) ddl_local_reduce_kernel(const __g
   }
 }
 
+// K5 through the TMA ring: every CTA streams chunks (g input segments of CB bytes each,
+// bulk-copied into a 2 x 48 KiB shared-memory ring by one elected thread, mbarrier
+// expect-tx), folds them in ascending j from shared memory and streams the result out.
+// Chunk k of the vector goes to CTA k mod grid.  The ragged end (< 16 B) is element-wise.
+template <typename T>
+__global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_local_reduce_tma_kernel(
+    const __grid_constant__ LRParams p) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = Tr<T>::W;
+  extern __shared__ __align__(128) char dsmem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dsmem + (size_t)kStages * kStageBytes);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t CB = (kStageBytes / (uint32_t)p.g) & ~15u;
+  const uint64_t vbytes = (p.n / W) * 16ull;              // whole vectors
+  const uint64_t nchunks = (vbytes + CB - 1) / CB;
+  const bool do_scale = p.scale != 1.0f;
+  // this CTA's chunks: blockIdx.x, blockIdx.x + gridDim.x, ...
+  const uint64_t mine = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto issue = [&](uint64_t k) {  // k-th chunk of this CTA -> stage k % kStages
+    const uint64_t chunk = blockIdx.x + k * gridDim.x;
+    const uint64_t off = chunk * CB;
+    const uint32_t bytes = (uint32_t)(vbytes - off < CB ? vbytes - off : CB);
+    const int st = (int)(k % kStages);
+    char* sb = dsmem + (size_t)st * kStageBytes;
+    mbar_arm(&bar[st], bytes * (uint32_t)p.g);
+    for (int j = 0; j < p.g; ++j)
+      tma_load(sb + (size_t)j * CB, static_cast<const char*>(p.in[j]) + off, bytes, &bar[st]);
+  };
+  if (threadIdx.x == 0)
+    for (uint64_t k = 0; k < mine && k < (uint64_t)kStages; ++k) issue(k);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const uint64_t chunk = blockIdx.x + k * gridDim.x;
+    const uint64_t off = chunk * CB;
+    const uint32_t bytes = (uint32_t)(vbytes - off < CB ? vbytes - off : CB);
+    const int st = (int)(k % kStages);
+    const char* sb = dsmem + (size_t)st * kStageBytes;
+    mbar_wait(&bar[st], (uint32_t)((k / kStages) & 1u));
+    char* pd = static_cast<char*>(p.out) + off;
+    for (uint32_t i = threadIdx.x; i < bytes / 16u; i += blockDim.x) {
+      A acc[W];
+      unpack<T>(*reinterpret_cast<const uint4*>(sb + (size_t)i * 16), acc);
+      for (int j = 1; j < p.g; ++j) {
+        A y[W];
+        unpack<T>(*reinterpret_cast<const uint4*>(sb + (size_t)j * CB + (size_t)i * 16), y);
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[q] = Tr<T>::add(acc[q], y[q]);
+      }
+      if (do_scale) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[q] = Tr<T>::mul(acc[q], p.scale);
+      }
+      __stcs(reinterpret_cast<uint4*>(pd + (size_t)i * 16), pack<T>(acc));
+    }
+    __syncthreads();  // stage st consumed
+    if (threadIdx.x == 0 && k + kStages < mine) issue(k + kStages);
+  }
+  if (blockIdx.x == 0) {  // the last n % W elements
+    const uint64_t e = (p.n / W) * W + threadIdx.x;
+    if (e < p.n) {
+      A a = Tr<T>::to(ld_elem<T>(static_cast<const char*>(p.in[0]) + e * sizeof(T)));
+      for (int j = 1; j < p.g; ++j)
+        a = Tr<T>::add(a, Tr<T>::to(ld_elem<T>(static_cast<const char*>(p.in[j]) + e * sizeof(T))));
+      if (do_scale) a = Tr<T>::mul(a, p.scale);
+      st_elem<T>(static_cast<char*>(p.out) + e * sizeof(T), Tr<T>::from(a));
+    }
+  }
+}
+
 }  // namespace ddl

@@ -1069,6 +1069,18 @@ ddl_result_t ddl_local_reduce(const void* const* ins, int g, void* out, size_t c
   int dev = 0, sms = 148;
   DDL_CUDA(cudaGetDevice(&dev));
   DDL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // large aligned reductions (>= 32 MiB out) stream through the TMA ring: +2-6% at 64-256 MiB,
+  // slower below (scripts/k5_bench.py); DDL_LR_NO_TMA=1 forces the register path
+  if (vec && count * elem_size(dt) >= (32u << 20) && env_size("DDL_LR_NO_TMA", 0) == 0) {
+    const void* tfn = dt == DDL_INT32 ? (const void*)ddl_local_reduce_tma_kernel<int32_t>
+                      : dt == DDL_FLOAT32 ? (const void*)ddl_local_reduce_tma_kernel<float>
+                                          : (const void*)ddl_local_reduce_tma_kernel<__nv_bfloat16>;
+    const int per_sm = blocks_per_sm(tfn, kTmaSmem);
+    void* targs[] = {&p};
+    DDL_CUDA(cudaLaunchKernel(tfn, dim3((unsigned)(per_sm * sms)), dim3(kThreads), targs, kTmaSmem,
+                              static_cast<cudaStream_t>(stream)));
+    return DDL_SUCCESS;
+  }
   const int W = vec ? 16 / elem_size(dt) : 1;
   const uint64_t items = (count + W - 1) / W;
   uint64_t grid = (uint64_t)blocks_per_sm(fn) * sms;

@@ -149,7 +149,7 @@ def test_reduce_scatter_allgather(P, dims):
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
 def test_local_reduce(dtype):
     for g in (1, 2, 3, 8, 13):
-        for n in (1, 1000, (1 << 20) + 5):
+        for n in (1, 1000, (1 << 20) + 5) + (((40 << 20) // 4 + 3,) if g in (3, 8) else ()):
             ins = si.rank_buffers(dtype, KIND[dtype], n, g, seed=g * 7 + n)
             scales = [1.0] if dtype == "int32" else [1.0, 0.125, 1.0 / 3.0]
             for s in scales:
