@@ -72,9 +72,13 @@ typedef enum {
 typedef enum { DDL_INT32 = 0, DDL_FLOAT32 = 1, DDL_BFLOAT16 = 2 } ddl_dtype_t;
 typedef enum { DDL_SUM = 0, DDL_AVG = 1 } ddl_op_t;
 
-/* Implementation choice per call ("mix-and-match", P:L54 (3)).  AUTO picks ONESHOT for
- * messages <= the one-shot threshold, HIER otherwise.  Both compute the same F_dims. */
-typedef enum { DDL_ALGO_AUTO = 0, DDL_ALGO_HIER = 1, DDL_ALGO_ONESHOT = 2 } ddl_algo_t;
+/* Implementation choice per call ("mix-and-match", P:L54 (3)).  AUTO picks, by message
+ * size: LL (multi-process comms only, <= the LL threshold, default 64 KiB: inputs pushed to
+ * every peer with the call counter in every 64-bit word, no barrier), ONESHOT (<= the
+ * one-shot threshold: every rank reads all inputs), HIER otherwise.  All three compute the
+ * same F_dims.  LL forced on a message that does not fit its receive slots (sized from the
+ * LL threshold at init) or on a loopback comm falls through to the AUTO rules. */
+typedef enum { DDL_ALGO_AUTO = 0, DDL_ALGO_HIER = 1, DDL_ALGO_ONESHOT = 2, DDL_ALGO_LL = 3 } ddl_algo_t;
 
 /* ------------------------------------------------------------------ host-only helpers */
 /* These never touch the GPU; they expose the planner the kernels use, for tests.       */
@@ -161,6 +165,12 @@ ddl_result_t ddl_async_error(ddl_comm_t comm);
 
 /* Algorithm override: algo, and the one-shot threshold in bytes (AUTO only). */
 ddl_result_t ddl_set_algo(ddl_comm_t comm, ddl_algo_t algo, size_t oneshot_max_bytes);
+
+/* LL threshold in bytes for AUTO (default 65536, env DDL_LL_MAX_BYTES; 0 = never LL).  The
+ * receive slots are sized at ddl_init from the threshold then in force (2 * nranks * 2 *
+ * threshold bytes per rank), so raising it later only helps up to that size.  Every rank
+ * must set the same value (the algorithm is chosen locally from it). */
+ddl_result_t ddl_set_ll_max(ddl_comm_t comm, size_t ll_max_bytes);
 
 /* Barrier-spin timeout in milliseconds (default 10000; env DDL_TIMEOUT_MS). */
 ddl_result_t ddl_set_timeout(ddl_comm_t comm, uint64_t timeout_ms);

@@ -6,6 +6,8 @@
 //                      separated by 2L+1 per-CTA device barriers (K4).
 //   ddl_oneshot_kernel small messages: every rank reads all P inputs, folds them in the
 //                      nested order of the dims (same F_dims as the hierarchy), 2 barriers.
+//   ddl_ll_kernel      smallest messages across processes: inputs pushed with the epoch in
+//                      every 64-bit word (LL protocol), no barrier, same nested fold.
 //   ddl_local_reduce_kernel  K5: out = s * sum_j in_j over local buffers (HBM roofline).
 //
 // Work split (a4 "per-CTA slices"): a block of q elements is cut into nctas slices; CTA c
@@ -69,6 +71,8 @@ struct KParams {
   uint32_t sig;        // DDL_CHECK=1: signature of (count, dtype, op, algorithm); 0 = no check
   char* scratch[kMaxRanks];  // kScratch: each rank's one-shot scratch (two halves, by call parity)
   uint64_t scratch_half;     // bytes per half
+  char* ll[kMaxRanks];       // LL one-shot: each rank's receive region (two halves of P slots)
+  uint64_t ll_slot;          // bytes per source slot (half = P slots)
 };
 constexpr int kTraceEvents = 40;
 
@@ -961,6 +965,156 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_c
     else
       for (uint64_t x = eoff; x < hi; ++x) st_elem<T>(o + x * sizeof(T), Tr<T>::from(res[i][x - eoff]));
   }
+  rank_epoch_end(p, me, e, 0);
+}
+
+// ------------------------------------------------------------------------ LL one-shot (a9)
+// Small messages across processes ("LL-style flags carried in the
+// payload").  Every rank PUSHES its input to every peer as 16-byte lines of two 64-bit words
+// {data32 | epoch << 32}: a 64-bit aligned store is single-copy atomic, so a word whose high
+// half equals this call's epoch carries this call's data -- no flag barrier, no fence, one
+// NVLink crossing per value (the pull one-shot needs a barrier round trip, then a remote-read
+// round trip).  Each rank then polls its own receive slots and folds the P values of every
+// line in the nested order of the dims (nested_feed, the same F_dims as every other path).
+// Receive region: two halves by call parity, slot r of a half holds rank r's lines; a half
+// is rewritten two calls later, when every peer has provably finished reading it (to push
+// call e+2 a peer must have finished call e+1, which needed this rank's call-e+1 data, sent
+// only after this rank finished call e).  The region holds nothing but LL words, so a stale
+// word carries an older epoch (epochs start at 1; the region is zeroed at init).
+__device__ __forceinline__ void st_ll(char* p, uint64_t a, uint64_t b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_ll(const char* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+// The 8 data bytes of a line as Acc values (2 x 32-bit, or 4 x bf16).
+template <typename T>
+__device__ __forceinline__ void unpack8(uint32_t lo, uint32_t hi, typename Tr<T>::Acc* a) {
+  if constexpr (sizeof(T) == 2) {
+    a[0] = Tr<T>::to(lo & 0xFFFFu);
+    a[1] = Tr<T>::to(lo >> 16);
+    a[2] = Tr<T>::to(hi & 0xFFFFu);
+    a[3] = Tr<T>::to(hi >> 16);
+  } else {
+    a[0] = Tr<T>::to(lo);
+    a[1] = Tr<T>::to(hi);
+  }
+}
+
+// This thread's 8 data bytes of line i (a ragged last line element by element, zero padded
+// on the wire only).
+template <typename T>
+__device__ __forceinline__ void ll_load(const char* src, int nvalid, uint32_t* d) {
+  constexpr int NE = 8 / (int)sizeof(T);
+  d[0] = d[1] = 0u;
+  if (nvalid == NE) {
+    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(src));
+    d[0] = v.x;
+    d[1] = v.y;
+  } else {
+    for (int k = 0; k < nvalid; ++k) {
+      const uint32_t b = ld_elem<T>(src + k * sizeof(T));
+      if constexpr (sizeof(T) == 2) d[k >> 1] |= b << (16 * (k & 1));
+      else d[k] = b;
+    }
+  }
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(kThreads, 1) ddl_ll_kernel(const __grid_constant__ KParams p) {
+  using A = typename Tr<T>::Acc;
+  constexpr int NE = 8 / (int)sizeof(T);  // elements per 8 data bytes
+  constexpr int CH = 8;
+  const int me = p.rank;
+  const uint32_t e = rank_epoch_begin(p, me);
+  if (me == p.skip_rank) return;
+  const Topo& t = p.t;
+  const int P = t.P;
+  int gl[K], Gl[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    gl[j] = t.g[t.live[j]];
+    Gl[j] = t.G[t.live[j]];
+  }
+  const uint64_t nbytes = p.n * sizeof(T);
+  const uint64_t nlines = (nbytes + 7) / 8;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t half = (uint64_t)(e & 1u) * (uint64_t)P * p.ll_slot;
+  const char* in = static_cast<const char*>(p.cin[me]);
+  auto nvalid_of = [&](uint64_t i) {
+    const uint64_t left = (nbytes - i * 8) / sizeof(T);
+    return left < (uint64_t)NE ? (int)left : NE;
+  };
+  // 1. push: every line to every peer (fire and forget)
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlines; i += stride) {
+    uint32_t d[2];
+    ll_load<T>(in + i * 8, nvalid_of(i), d);
+    const uint64_t w0 = ((uint64_t)e << 32) | d[0], w1 = ((uint64_t)e << 32) | d[1];
+    for (int m = 0; m < P; ++m)
+      if (m != me) st_ll(p.ll[m] + half + (uint64_t)me * p.ll_slot + i * 16, w0, w1);
+  }
+  // 2. poll my receive slots, fold in the nested order, write (line i is written only by
+  //    this thread, after its own input bytes were read again)
+  int fail = 0;
+  uint64_t t0 = 0;
+  uint32_t spins = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlines && !fail; i += stride) {
+    const int nvalid = nvalid_of(i);
+    uint32_t d[2];
+    ll_load<T>(in + i * 8, nvalid, d);
+    const char* mine = p.ll[me] + half + i * 16;
+    A lvl[K][NE];
+    A res[NE];
+    for (int r0 = 0; r0 < P; r0 += CH) {
+      uint64_t a[CH], b[CH];
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {  // all loads of the chunk in flight at once
+        const int r = r0 + k;
+        if (r >= P) break;
+        if (r == me) {
+          a[k] = ((uint64_t)e << 32) | d[0];
+          b[k] = ((uint64_t)e << 32) | d[1];
+        } else {
+          ld_ll(mine + (uint64_t)r * p.ll_slot, a[k], b[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int r = r0 + k;
+        if (r >= P) break;
+        while (!fail && ((uint32_t)(a[k] >> 32) != e || (uint32_t)(b[k] >> 32) != e)) {
+          if ((++spins & 255u) == 0) {
+            const uint64_t now = globaltimer();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > p.timeout_ns) {
+              atomicCAS(p.err, 0, kErrTimeout);
+              fail = 1;
+            }
+          }
+          ld_ll(mine + (uint64_t)r * p.ll_slot, a[k], b[k]);
+        }
+        A x[NE];
+        unpack8<T>((uint32_t)a[k], (uint32_t)b[k], x);
+        nested_feed<T, K, NE>(p, gl, Gl, r, lvl, x, res);
+      }
+    }
+    if (fail) break;
+    char* o = static_cast<char*>(p.out[me]) + i * 8;
+    if (nvalid == NE) {
+      uint32_t w[2];
+      if constexpr (sizeof(T) == 2) {
+        w[0] = Tr<T>::from(res[0]) | (Tr<T>::from(res[1]) << 16);
+        w[1] = Tr<T>::from(res[2]) | (Tr<T>::from(res[3]) << 16);
+      } else {
+        w[0] = Tr<T>::from(res[0]);
+        w[1] = Tr<T>::from(res[1]);
+      }
+      *reinterpret_cast<uint2*>(o) = make_uint2(w[0], w[1]);
+    } else {
+      for (int k = 0; k < nvalid; ++k) st_elem<T>(o + k * sizeof(T), Tr<T>::from(res[k]));
+    }
+  }
+  if (__syncthreads_or(fail)) return;  // the call counter stays (like a failed barrier)
   rank_epoch_end(p, me, e, 0);
 }
 

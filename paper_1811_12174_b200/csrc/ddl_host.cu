@@ -73,7 +73,7 @@ struct Handle {  // exported per rank, all-gathered by the caller
   int32_t dims[kMaxDims];
   int32_t cmax;
   int32_t pad;
-  uint64_t flags_bytes, max_bytes, alloc_bytes, scratch_half;
+  uint64_t flags_bytes, max_bytes, alloc_bytes, scratch_half, ll_slot;
   char pci[32];
   cudaIpcMemHandle_t ipc;
 };
@@ -172,6 +172,10 @@ struct ddl_comm {
   char* stage_of(int r) const { return (r == rank ? alloc : peer_base[r]) + flags_bytes + max_bytes; }
   size_t scratch_half = 0;  // one-shot scratch: two halves after the staging area
   char* scratch_of(int r) const { return stage_of(r) + max_bytes; }
+  // LL receive region after the scratch: two halves of P slots of ll_slot bytes
+  size_t ll_max = 64 << 10;  // AUTO uses LL up to this message size (DDL_LL_MAX_BYTES, 0 = off)
+  size_t ll_slot = 0;
+  char* ll_of(int r) const { return scratch_of(r) + 2 * scratch_half; }
 };
 
 namespace {
@@ -202,9 +206,11 @@ void apply_env(ddl_comm* c) {
   c->use_stream = env_size("DDL_STREAM", 0) != 0;
   c->check = env_size("DDL_CHECK", 0) != 0;
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
+  c->ll_max = env_size("DDL_LL_MAX_BYTES", c->ll_max);
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
     else if (!std::strcmp(a, "oneshot")) c->algo = DDL_ALGO_ONESHOT;
+    else if (!std::strcmp(a, "ll")) c->algo = DDL_ALGO_LL;
     else c->algo = DDL_ALGO_AUTO;
   }
 }
@@ -243,7 +249,8 @@ struct Plan {
   int path = 2;  // hierarchical kernel variant: 0 element-wise, 1 register-staged, 2 TMA-staged,
                  // 3 TMA-staged with rank-level barriers and dynamic chunks
   bool oneshot = false;
-  int r = 1;  // one-shot: vectors per thread
+  bool ll = false;  // LL one-shot (multi-process small messages)
+  int r = 1;        // one-shot: vectors per thread
 };
 
 template <typename T>
@@ -267,6 +274,21 @@ const void* oneshot_fn_r(int K) {
 template <typename T>
 const void* oneshot_fn(int K, int R) {
   return R == 4 ? oneshot_fn_r<T, 4>(K) : R == 2 ? oneshot_fn_r<T, 2>(K) : oneshot_fn_r<T, 1>(K);
+}
+template <typename T>
+const void* ll_fn(int K) {
+  switch (K) {
+    case 1: return (const void*)ddl_ll_kernel<T, 1>;
+    case 2: return (const void*)ddl_ll_kernel<T, 2>;
+    case 3: return (const void*)ddl_ll_kernel<T, 3>;
+    case 4: return (const void*)ddl_ll_kernel<T, 4>;
+    default: return nullptr;
+  }
+}
+const void* ll_fn_dt(ddl_dtype_t dt, int K) {
+  if (dt == DDL_INT32) return ll_fn<int32_t>(K);
+  if (dt == DDL_FLOAT32) return ll_fn<float>(K);
+  return ll_fn<__nv_bfloat16>(K);
 }
 const void* hier_fn_dt(ddl_dtype_t dt, int path) {
   if (dt == DDL_INT32) return hier_fn<int32_t>(path);
@@ -334,6 +356,29 @@ bool plan_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
   return false;
 }
 
+// LL one-shot: multi-process only, 8 data bytes per thread and line, the message must fit a
+// receive slot (16 bytes per 8 data bytes); not with DDL_CHECK (no barrier to carry the
+// signature).  ALGO_LL forces it wherever it fits, AUTO up to ll_max bytes.
+bool use_ll(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
+  if (c->loopback || c->P < 2 || c->check) return false;
+  if (c->algo != DDL_ALGO_LL && c->algo != DDL_ALGO_AUTO) return false;
+  const uint64_t bytes = n * (uint64_t)elem_size(dt);
+  if (c->algo == DDL_ALGO_AUTO && bytes > c->ll_max) return false;
+  const uint64_t lines = (bytes + 7) / 8;
+  if (lines * 16 > c->ll_slot) return false;
+  const void* fn = ll_fn_dt(dt, c->topo.nlive);
+  if (!fn) return false;
+  uint64_t ctas = (lines + kThreads - 1) / kThreads;  // one line per thread, grid-stride past the cap
+  const uint64_t cap = (uint64_t)cap_per_rank(c, fn);
+  if (ctas > cap) ctas = cap;
+  pl->ll = true;
+  pl->oneshot = false;
+  pl->q = 0;
+  pl->slice = 0;
+  pl->nctas = (int)ctas;
+  return true;
+}
+
 bool use_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
   if (c->P < 2 || c->algo == DDL_ALGO_HIER) return false;
   if (!c->loopback && n * (uint64_t)elem_size(dt) > c->scratch_half) return false;  // scratch-bound
@@ -366,20 +411,22 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
   if (c->check && !c->loopback) {  // FNV-1a over what every rank must agree on
     uint32_t h = 2166136261u;
     const uint64_t vals[] = {p.n, (uint64_t)dt, (uint64_t)p.op, (uint64_t)p.mode, (uint64_t)pl.oneshot,
-                             (uint64_t)pl.path, (uint64_t)pl.nctas, p.q};
+                             (uint64_t)pl.path, (uint64_t)pl.nctas, p.q, (uint64_t)pl.ll};
     for (uint64_t v : vals)
       for (int b = 0; b < 8; ++b) h = (h ^ (uint32_t)((v >> (8 * b)) & 0xFF)) * 16777619u;
     p.sig = h | 1u;
   }
-  const void* fn = pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive, pl.r) : hier_fn_dt(dt, pl.path);
+  const void* fn = pl.ll        ? ll_fn_dt(dt, c->topo.nlive)
+                   : pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive, pl.r)
+                                : hier_fn_dt(dt, pl.path);
   if (!fn) return DDL_ERR_UNSUPPORTED;
-  const size_t smem = pl.oneshot ? 0 : hier_smem(pl.path);
+  const size_t smem = (pl.oneshot || pl.ll) ? 0 : hier_smem(pl.path);
   blocks_per_sm(fn, smem);  // sets the dynamic shared-memory attribute once
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void* args[] = {const_cast<KParams*>(&p)};
   if (std::getenv("DDL_DEBUG"))
     std::fprintf(stderr, "[ddl] %s n=%llu q=%llu slice=%llu ctas=%d path=%d mode=%d P=%d loopback=%d\n",
-                 pl.oneshot ? "oneshot" : "hier", (unsigned long long)p.n, (unsigned long long)p.q,
+                 pl.ll ? "ll" : pl.oneshot ? "oneshot" : "hier", (unsigned long long)p.n, (unsigned long long)p.q,
                  (unsigned long long)p.slice, pl.nctas, pl.path, p.mode, c->P, (int)c->loopback);
   if (c->loopback) {
     DDL_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pl.nctas, c->P), dim3(kThreads), args, smem, s));
@@ -537,9 +584,12 @@ ddl_result_t ddl_init(ddl_comm_t* comm, int rank, int nranks, const int* dims, i
   c->rank = rank;
   c->max_bytes = (max_bytes + 4095) / 4096 * 4096;
   c->scratch_half = ((c->oneshot_max > (512u << 10) ? c->oneshot_max : (512u << 10)) + 4095) / 4096 * 4096;
-  c->alloc_bytes = c->flags_bytes + 2 * c->max_bytes + 2 * c->scratch_half;
+  c->ll_slot = (2 * c->ll_max + 4095) / 4096 * 4096;  // 16 bytes per 8 data bytes
+  c->alloc_bytes = c->flags_bytes + 2 * c->max_bytes + 2 * c->scratch_half + 2 * (size_t)nranks * c->ll_slot;
   cudaError_t e = cudaMalloc(&c->alloc, c->alloc_bytes);
   if (e == cudaSuccess) e = cudaMemset(c->alloc, 0, c->flags_bytes);
+  // LL words carry the call epoch (>= 1): the region must start with none that could match
+  if (e == cudaSuccess && c->ll_slot) e = cudaMemset(c->ll_of(rank), 0, 2 * (size_t)nranks * c->ll_slot);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -569,6 +619,7 @@ ddl_result_t ddl_export_handle(ddl_comm_t c, void* out) {
   h.flags_bytes = c->flags_bytes;
   h.max_bytes = c->max_bytes;
   h.scratch_half = c->scratch_half;
+  h.ll_slot = c->ll_slot;
   h.alloc_bytes = c->alloc_bytes;
   DDL_ON_DEVICE(c->device);
   DDL_CUDA(cudaDeviceGetPCIBusId(h.pci, sizeof(h.pci), c->device));
@@ -586,7 +637,7 @@ ddl_result_t ddl_connect(ddl_comm_t c, const void* all_handles) {
     const Handle& h = hs[m];
     if (h.magic != kMagic || h.rank != m) return DDL_ERR_INVALID_ARGUMENT;
     if (h.nranks != c->P || h.ndims != c->ndims || h.cmax != c->cmax || h.flags_bytes != c->flags_bytes ||
-        h.max_bytes != c->max_bytes || h.scratch_half != c->scratch_half)
+        h.max_bytes != c->max_bytes || h.scratch_half != c->scratch_half || h.ll_slot != c->ll_slot)
       return DDL_ERR_MISMATCH;
     for (int d = 0; d < c->ndims; ++d)
       if (h.dims[d] != c->dims[d]) return DDL_ERR_MISMATCH;
@@ -637,6 +688,13 @@ ddl_result_t ddl_allreduce(ddl_comm_t c, void* buf, size_t count, ddl_dtype_t dt
   DDL_ON_DEVICE(c->device);
   KParams p = base_params(c, count, op);
   Plan pl;
+  if (use_ll(c, count, dt, &pl)) {
+    p.cin[c->rank] = buf;
+    p.out[c->rank] = buf;
+    for (int m = 0; m < c->P; ++m) p.ll[m] = c->ll_of(m);
+    p.ll_slot = c->ll_slot;
+    return launch(c, p, pl, dt, stream);
+  }
   const bool one = use_oneshot(c, count, dt, &pl);
   if (!one) pl = plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true);
   p.q = pl.q;
@@ -738,9 +796,15 @@ ddl_result_t ddl_async_error(ddl_comm_t c) {
 }
 
 ddl_result_t ddl_set_algo(ddl_comm_t c, ddl_algo_t algo, size_t oneshot_max_bytes) {
-  if (!c || algo < DDL_ALGO_AUTO || algo > DDL_ALGO_ONESHOT) return DDL_ERR_INVALID_ARGUMENT;
+  if (!c || algo < DDL_ALGO_AUTO || algo > DDL_ALGO_LL) return DDL_ERR_INVALID_ARGUMENT;
   c->algo = algo;
   c->oneshot_max = oneshot_max_bytes;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_set_ll_max(ddl_comm_t c, size_t ll_max_bytes) {
+  if (!c) return DDL_ERR_INVALID_ARGUMENT;
+  c->ll_max = ll_max_bytes;  // eligibility is also bounded by the receive slot size from init
   return DDL_SUCCESS;
 }
 
@@ -753,13 +817,14 @@ ddl_result_t ddl_set_timeout(ddl_comm_t c, uint64_t timeout_ms) {
 ddl_algo_t ddl_algo_for(ddl_comm_t c, size_t count, ddl_dtype_t dt) {
   if (!c || !valid_dtype(dt)) return DDL_ALGO_AUTO;
   Plan pl;
+  if (use_ll(c, count, dt, &pl)) return DDL_ALGO_LL;
   return use_oneshot(c, count, dt, &pl) ? DDL_ALGO_ONESHOT : DDL_ALGO_HIER;
 }
 
 int ddl_ctas_for(ddl_comm_t c, size_t count, ddl_dtype_t dt) {
   if (!c || !valid_dtype(dt) || count == 0) return 0;
   Plan pl;
-  if (use_oneshot(c, count, dt, &pl)) return pl.nctas;
+  if (use_ll(c, count, dt, &pl) || use_oneshot(c, count, dt, &pl)) return pl.nctas;
   return plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true).nctas;
 }
 
@@ -785,7 +850,8 @@ ddl_result_t ddl_debug_connect_local(ddl_comm_t* comms, int nranks) {
     const ddl_comm* c = comms[r];
     if (!c || c->loopback || c->rank != r || c->P != nranks) return DDL_ERR_INVALID_ARGUMENT;
     if (c->ndims != comms[0]->ndims || c->max_bytes != comms[0]->max_bytes || c->cmax != comms[0]->cmax ||
-        c->device != comms[0]->device || c->scratch_half != comms[0]->scratch_half)
+        c->device != comms[0]->device || c->scratch_half != comms[0]->scratch_half ||
+        c->ll_slot != comms[0]->ll_slot)
       return DDL_ERR_MISMATCH;
     for (int d = 0; d < c->ndims; ++d)
       if (c->dims[d] != comms[0]->dims[d]) return DDL_ERR_MISMATCH;

@@ -28,7 +28,7 @@ SUCCESS, ERR_INVALID_ARGUMENT, ERR_BAD_DIMS, ERR_UNSUPPORTED, ERR_CUDA, ERR_NO_P
     ERR_NOT_CONNECTED, ERR_TOO_LARGE, ERR_TIMEOUT, ERR_MISMATCH = range(10)
 INT32, FLOAT32, BFLOAT16 = 0, 1, 2
 SUM, AVG = 0, 1
-ALGO_AUTO, ALGO_HIER, ALGO_ONESHOT = 0, 1, 2
+ALGO_AUTO, ALGO_HIER, ALGO_ONESHOT, ALGO_LL = 0, 1, 2, 3
 MAX_RANKS = 16
 
 DTYPE_CODES = {"int32": INT32, "float32": FLOAT32, "bfloat16": BFLOAT16}
@@ -71,6 +71,7 @@ def _load() -> ctypes.CDLL:
         "ddl_allgather": (c_int, [c_void, c_void, c_void, c_size, c_int, c_void]),
         "ddl_async_error": (c_int, [c_void]),
         "ddl_set_algo": (c_int, [c_void, c_int, c_size]),
+        "ddl_set_ll_max": (c_int, [c_void, c_size]),
         "ddl_set_timeout": (c_int, [c_void, c_u64]),
         "ddl_algo_for": (c_int, [c_void, c_size, c_int]),
         "ddl_ctas_for": (c_int, [c_void, c_size, c_int]),
@@ -308,6 +309,12 @@ class Comm:
     def set_algo(self, algo: int, oneshot_max_bytes: int = 512 << 10) -> None:
         _check(_lib.ddl_set_algo(self.h, algo, oneshot_max_bytes), "ddl_set_algo")
 
+    def set_ll_max(self, ll_max_bytes: int) -> None:
+        _check(_lib.ddl_set_ll_max(self.h, ll_max_bytes), "ddl_set_ll_max")
+
+    def algo_for(self, count: int, dtype: str) -> int:
+        return _lib.ddl_algo_for(self.h, count, DTYPE_CODES[dtype])
+
     def async_error(self) -> int:
         return _lib.ddl_async_error(self.h)
 
@@ -504,6 +511,13 @@ class InProcessGroup:
     def set_algo(self, algo: int, oneshot_max_bytes: int = 512 << 10) -> None:
         for h in self.hs:
             _check(_lib.ddl_set_algo(h, algo, oneshot_max_bytes), "ddl_set_algo")
+
+    def set_ll_max(self, ll_max_bytes: int) -> None:
+        for h in self.hs:
+            _check(_lib.ddl_set_ll_max(h, ll_max_bytes), "ddl_set_ll_max")
+
+    def algo_for(self, count: int, dtype: str) -> int:
+        return _lib.ddl_algo_for(self.hs[0], count, DTYPE_CODES[dtype])
 
     def async_error(self) -> int:
         return max(_lib.ddl_async_error(h) for h in self.hs)

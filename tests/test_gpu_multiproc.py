@@ -47,6 +47,19 @@ def _rank_main(rank, world, port, q, env, dims):
             comm.all_reduce(st, op)
             torch.cuda.synchronize()
             res[dtype] = (same_bits(to_host(zc), want), same_bits(to_host(st), want))
+        # small messages: the LL one-shot (AUTO up to 64 KiB), pushed through the IPC mapping
+        ll_ok = []
+        for dtype, op in (("float32", "avg"), ("int32", "sum"), ("bfloat16", "sum")):
+            kind = "fullrange" if dtype == "int32" else "normal"
+            for n in (1, 3, 1001, 16_384):
+                ll_ok.append(comm.algo_for(n, dtype) == ddl.ALGO_LL)
+                bufs = si.rank_buffers(dtype, kind, n, world, seed=n)
+                want = oracle.allreduce(bufs, dims, dtype, op)[rank]
+                st = to_dev(bufs[rank], dtype)
+                comm.all_reduce(st, op)
+                torch.cuda.synchronize()
+                ll_ok.append(bool(same_bits(to_host(st), want)))
+        res["ll"] = tuple(ll_ok)
         # staged message larger than the workspace: reduced in pieces (ddl.Comm.all_reduce)
         big = si.rank_buffers("float32", "normal", 6_000_001, world, seed=5)
         want = oracle.allreduce_sampled(big, dims, "float32", "avg", np.arange(0, 6_000_001, 997))
@@ -96,5 +109,5 @@ def test_processes_ipc_one_gpu(world, dims, env):
     for r in range(world):
         assert "exc" not in out[r], out[r]
         assert out[r]["err"] == 0
-        for dtype in ("float32", "int32", "bfloat16", "big", "registered"):
+        for dtype in ("float32", "int32", "bfloat16", "ll", "big", "registered"):
             assert all(out[r][dtype]), (r, dtype)
