@@ -40,18 +40,22 @@ for (P, dims), force in runs:
 os.environ["DDL_TMA_MIN_SLICE_BYTES"] = "0"
 g = ddl.InProcessGroup(2, [2], max_bytes=1 << 20)
 os.environ.pop("DDL_TMA_MIN_SLICE_BYTES", None)
-for n in (5, 4099):
-    zc = [g.buffer(r, n, torch.float32) for r in range(2)]
-    for r in range(2):
-        zc[r].fill_(r + 1)
-    st = [torch.full((n,), r + 1.0, device="cuda") for r in range(2)]
-    g.all_reduce(zc)
-    g.all_reduce(st)
-    check(zc, 3)
-    check(st, 3)
+for algo in (ddl.ALGO_LL, ddl.ALGO_ONESHOT, ddl.ALGO_HIER):
+    g.set_algo(algo, 1 << 19)
+    for n in (5, 4099):
+        for dt in (torch.float32, torch.bfloat16):
+            zc = [g.buffer(r, n, dt) for r in range(2)]
+            for r in range(2):
+                zc[r].fill_(r + 1)
+            st = [torch.full((n,), r + 1.0, dtype=dt, device="cuda") for r in range(2)]
+            g.all_reduce(zc)
+            g.all_reduce(st)
+            check(zc, 3)
+            check(st, 3)
 g.finalize()
-ins = [torch.full((1001,), float(j), device="cuda") for j in range(3)]
-out = torch.empty(1001, device="cuda")
-ddl.local_reduce(ins, out, 0.5)
-check([out], 1.5)
+for n in (1001, (32 << 20) // 4 + 3):   # register path, then the TMA-ring path (>= 32 MiB)
+    ins = [torch.full((n,), float(j), device="cuda") for j in range(3)]
+    out = torch.empty(n, device="cuda")
+    ddl.local_reduce(ins, out, 0.5)
+    check([out], 1.5)
 print("sanitize_check ok")
