@@ -66,7 +66,7 @@ typedef enum {
   DDL_ERR_NOT_CONNECTED = 6,    /* collective called before ddl_connect                     */
   DDL_ERR_TOO_LARGE = 7,        /* message exceeds the workspace on a staged path           */
   DDL_ERR_TIMEOUT = 8,          /* (async) a device barrier waited longer than the timeout  */
-  DDL_ERR_MISMATCH = 9          /* handles from ranks with different nranks/dims            */
+  DDL_ERR_MISMATCH = 9          /* ranks disagree: handles (nranks/dims/sizes) at connect, or (async, DDL_CHECK=1) the call signature */
 } ddl_result_t;
 
 typedef enum { DDL_INT32 = 0, DDL_FLOAT32 = 1, DDL_BFLOAT16 = 2 } ddl_dtype_t;

@@ -474,7 +474,7 @@ ddl_result_t local_copy(const void* src, void* dst, size_t count, ddl_dtype_t dt
 
 extern "C" {
 
-int ddl_version(void) { return 100; }
+int ddl_version(void) { return 101; }  // 1.01: LL one-shot, ddl_set_ll_max
 
 const char* ddl_result_string(ddl_result_t r) {
   switch (r) {
@@ -487,7 +487,7 @@ const char* ddl_result_string(ddl_result_t r) {
     case DDL_ERR_NOT_CONNECTED: return "not connected";
     case DDL_ERR_TOO_LARGE: return "message larger than the workspace";
     case DDL_ERR_TIMEOUT: return "device barrier timeout";
-    case DDL_ERR_MISMATCH: return "handle mismatch between ranks";
+    case DDL_ERR_MISMATCH: return "ranks disagree (handles at connect, or the call signature with DDL_CHECK=1)";
   }
   return "unknown";
 }
