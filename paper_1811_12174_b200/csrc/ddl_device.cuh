@@ -98,6 +98,16 @@ struct LRParams {
   float scale;
 };
 
+// Programmatic dependent launch: every kernel is launched with programmatic stream
+// serialisation allowed, so its CTAs may be scheduled while the previous kernel on the
+// stream drains.  griddepcontrol.wait blocks until that kernel has completed and its memory
+// is visible -- before any global access here -- and launch_dependents lets the next
+// kernel's CTAs be scheduled as soon as SMs free up (they wait the same way).
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------ element traits
 template <typename T> struct Tr;
 template <> struct Tr<int32_t> {  // int32: wrapping adds in uint32
@@ -755,6 +765,7 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
 // loads, 2 = 16-byte TMA-staged (default), 4 = TMA-staged with work stealing.
 template <typename T, int PATH>
 __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
+  pdl_begin();
   constexpr bool VEC = PATH >= 1;
   constexpr bool TMA = PATH >= 2;
   constexpr bool STEAL = PATH == 4;
@@ -881,6 +892,7 @@ __device__ __forceinline__ void nested_feed(const KParams& p, const int* gl, con
 
 template <typename T, int K, int R>
 __global__ void __launch_bounds__(kThreads, 1) ddl_oneshot_kernel(const __grid_constant__ KParams p) {
+  pdl_begin();
   using A = typename Tr<T>::Acc;
   constexpr int W = Tr<T>::W;
   constexpr int CH = 8;
@@ -1022,6 +1034,7 @@ __device__ __forceinline__ void ll_load(const char* src, int nvalid, uint32_t* d
 
 template <typename T, int K>
 __global__ void __launch_bounds__(kThreads, 1) ddl_ll_kernel(const __grid_constant__ KParams p) {
+  pdl_begin();
   using A = typename Tr<T>::Acc;
   constexpr int NE = 8 / (int)sizeof(T);  // elements per 8 data bytes
   constexpr int CH = 8;
@@ -1123,6 +1136,7 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_ll_kernel(const __grid_consta
 // loads in flight per thread, streaming cache hints (every byte is touched once).
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kThreads, 2) ddl_local_reduce_kernel(const __grid_constant__ LRParams p) {
+  pdl_begin();
   using A = typename Tr<T>::Acc;
   constexpr int W = VEC ? Tr<T>::W : 1;
   constexpr int CH = 8;
@@ -1180,6 +1194,7 @@ __global__ void __launch_bounds__(kThreads, 2) ddl_local_reduce_kernel(const __g
 template <typename T>
 __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_local_reduce_tma_kernel(
     const __grid_constant__ LRParams p) {
+  pdl_begin();
   using A = typename Tr<T>::Acc;
   constexpr int W = Tr<T>::W;
   extern __shared__ __align__(128) char dsmem[];

@@ -729,6 +729,7 @@ __device__ void dyn_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp,
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_dyn_kernel(const __grid_constant__ KParams p) {
+  pdl_begin();
   const int me = p.loopback ? (int)blockIdx.y : p.rank;
   uint32_t* rs = rank_state(p, me);
   const uint32_t e = rank_epoch_begin(p, me);

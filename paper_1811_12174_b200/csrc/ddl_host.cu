@@ -145,6 +145,7 @@ struct ddl_comm {
   int gpu_share = 1;        // ranks sharing this GPU (loopback: P; in-process test groups: P)
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
+  bool use_pdl = true;  // programmatic dependent launch (DDL_PDL=0: plain stream order)
 
   uint32_t* flags_of(int r) const {
     if (loopback) return reinterpret_cast<uint32_t*>(lb_flags + (size_t)r * flags_bytes);
@@ -180,6 +181,36 @@ struct ddl_comm {
 
 namespace {
 
+// Launch with the optional cooperative (loopback: all P x nctas CTAs co-resident) and
+// programmatic-dependent-launch attributes (every kernel starts with pdl_begin()).
+cudaError_t launch_ex(const void* fn, dim3 grid, size_t smem, cudaStream_t s, void** args, bool coop, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+bool pdl_default() {
+  static const bool on = env_size("DDL_PDL", 1) != 0;
+  return on;
+}
+
 // Resident CTAs (kThreads each) per SM for a kernel, cached.
 int blocks_per_sm(const void* fn, size_t smem = 0) {
   static std::mutex mu;
@@ -207,6 +238,7 @@ void apply_env(ddl_comm* c) {
   c->check = env_size("DDL_CHECK", 0) != 0;
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   c->ll_max = env_size("DDL_LL_MAX_BYTES", c->ll_max);
+  c->use_pdl = env_size("DDL_PDL", 1) != 0;
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
     else if (!std::strcmp(a, "oneshot")) c->algo = DDL_ALGO_ONESHOT;
@@ -429,9 +461,9 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
                  pl.ll ? "ll" : pl.oneshot ? "oneshot" : "hier", (unsigned long long)p.n, (unsigned long long)p.q,
                  (unsigned long long)p.slice, pl.nctas, pl.path, p.mode, c->P, (int)c->loopback);
   if (c->loopback) {
-    DDL_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pl.nctas, c->P), dim3(kThreads), args, smem, s));
+    DDL_CUDA(launch_ex(fn, dim3(pl.nctas, c->P), smem, s, args, true, c->use_pdl));
   } else {
-    DDL_CUDA(cudaLaunchKernel(fn, dim3(pl.nctas), dim3(kThreads), args, smem, s));
+    DDL_CUDA(launch_ex(fn, dim3(pl.nctas), smem, s, args, false, c->use_pdl));
   }
   return DDL_SUCCESS;
 }
@@ -1143,8 +1175,8 @@ ddl_result_t ddl_local_reduce(const void* const* ins, int g, void* out, size_t c
                                           : (const void*)ddl_local_reduce_tma_kernel<__nv_bfloat16>;
     const int per_sm = blocks_per_sm(tfn, kTmaSmem);
     void* targs[] = {&p};
-    DDL_CUDA(cudaLaunchKernel(tfn, dim3((unsigned)(per_sm * sms)), dim3(kThreads), targs, kTmaSmem,
-                              static_cast<cudaStream_t>(stream)));
+    DDL_CUDA(launch_ex(tfn, dim3((unsigned)(per_sm * sms)), kTmaSmem, static_cast<cudaStream_t>(stream), targs,
+                       false, pdl_default()));
     return DDL_SUCCESS;
   }
   const int W = vec ? 16 / elem_size(dt) : 1;
@@ -1154,7 +1186,7 @@ ddl_result_t ddl_local_reduce(const void* const* ins, int g, void* out, size_t c
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
   void* args[] = {&p};
-  DDL_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kThreads), args, 0, static_cast<cudaStream_t>(stream)));
+  DDL_CUDA(launch_ex(fn, dim3((unsigned)grid), 0, static_cast<cudaStream_t>(stream), args, false, pdl_default()));
   return DDL_SUCCESS;
 }
 
