@@ -148,24 +148,25 @@ def loopback_hbm_bytes(n: int, P: int, dims, w: int) -> int:
 
 
 # ----------------------------------------------------------------------------- cpu baseline
-def oracle_baseline(P: int, dims, budget_s: float = 12.0):
-    """The oracle as it stands, on a bounded sample of the workload (host cores)."""
+def oracle_baseline(P: int, dims, host, budget_s: float = 10.0):
+    """The oracle as it stands, on the host cores: whole steps of the same workload (every
+    bucket of the gradient set, all P simulated ranks), repeated while under budget_s."""
     import oracle
-    n = 4 << 20
-    bufs = [si.resnet50_bucket(1, r)[:n] for r in range(P)]
-    S = n * 4
+    nb = len(host[0])
+    S = sum(h.size for h in host[0]) * 4
     t0 = time.perf_counter()
     reps = 0
     while True:
-        oracle.allreduce(bufs, dims, "float32", "avg")
+        for b in range(nb):
+            oracle.allreduce([host[r][b] for r in range(P)], dims, "float32", "avg")
         reps += 1
         el = time.perf_counter() - t0
-        if el > budget_s or reps >= 8:
+        if el > budget_s:
             break
     t = el / reps
     return {"value": S * 2 * (P - 1) / P / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"{reps} oracle all-reduce(s) of 4M fp32 elements x {P} simulated ranks "
-                      f"(first 16 MiB of ResNet-50 bucket 1), dims {dims}, avg; numpy single-threaded",
+            "sample": f"{reps} whole step(s): the {nb} ResNet-50 buckets ({S} B per rank) x {P} simulated "
+                      f"ranks, dims {dims}, avg, {t:.2f} s per step; numpy single-threaded",
             "host_cpus": len(os.sched_getaffinity(0))}
 
 
@@ -179,8 +180,8 @@ def run_reference(args):
     # the ddl arm's configuration: N = 1 simulates the 8 ranks of 2x4; N > 1 runs N ranks
     P = 8 if args.gpus == 1 else args.gpus
     dims = oracle.parse_dims(args.dims or DIMS_FOR_N.get(args.gpus, str(args.gpus)))
-    n = 1 << 20
-    bufs = [si.resnet50_bucket(1, r)[:n] for r in range(P)]
+    bufs = [si.resnet50_bucket(1, r) for r in range(P)]   # bucket 1 whole (7.9M fp32 per rank)
+    n = bufs[0].size
     for _ in range(args.warmup):
         oracle.allreduce(bufs, dims, "float32", "avg")
     t0 = time.perf_counter()
@@ -191,12 +192,12 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"resnet50-grad-set sample: 1M fp32 x {P} simulated ranks, dims "
+            "config": {"workload": f"resnet50-grad-set sample: bucket 1 ({n} fp32) x {P} simulated ranks, dims "
                                    + "x".join(map(str, dims[::-1])) + ", avg",
                        "dims": "x".join(map(str, dims[::-1])), "n_ranks": P},
             "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": "each step: one oracle all-reduce of the first 1M elements of "
-                                       f"ResNet-50 bucket 1 on {P} simulated ranks"},
+                             "sample": f"each step: one oracle all-reduce of ResNet-50 bucket 1 ({n} fp32) "
+                                       f"on {P} simulated ranks"},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -335,7 +336,7 @@ def run_loopback(args):
                          "unit": "GB/s", "frac": k5_gbs / hbm_peak},
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = oracle_baseline(P, dims)
+        line["cpu_baseline"] = oracle_baseline(P, dims, host)
     print(json.dumps(line), flush=True)
     lb.finalize()
 
