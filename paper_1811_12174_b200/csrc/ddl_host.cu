@@ -146,6 +146,9 @@ struct ddl_comm {
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
   bool use_pdl = true;  // programmatic dependent launch (DDL_PDL=0: plain stream order)
+  bool force_sys = false;  // DDL_FORCE_SYS_SCOPE=1: .sys flags even when every rank shares this GPU
+  bool debug = false;      // DDL_DEBUG: one stderr line per launch
+  int stream_every = 1;    // DDL_STREAM_EVERY (PATH 5)
 
   uint32_t* flags_of(int r) const {
     if (loopback) return reinterpret_cast<uint32_t*>(lb_flags + (size_t)r * flags_bytes);
@@ -239,6 +242,10 @@ void apply_env(ddl_comm* c) {
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   c->ll_max = env_size("DDL_LL_MAX_BYTES", c->ll_max);
   c->use_pdl = env_size("DDL_PDL", 1) != 0;
+  c->force_sys = env_size("DDL_FORCE_SYS_SCOPE", 0) != 0;
+  c->debug = std::getenv("DDL_DEBUG") != nullptr;
+  c->stream_every = (int)env_size("DDL_STREAM_EVERY", 1);
+  if (c->stream_every < 1) c->stream_every = 1;
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
     else if (!std::strcmp(a, "oneshot")) c->algo = DDL_ALGO_ONESHOT;
@@ -424,7 +431,7 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
   p.t = c->topo;
   p.rank = c->rank;
   p.loopback = c->loopback ? 1 : 0;
-  p.gpu_scope = (c->gpu_share == c->P && !env_size("DDL_FORCE_SYS_SCOPE", 0)) ? 1 : 0;
+  p.gpu_scope = (c->gpu_share == c->P && !c->force_sys) ? 1 : 0;
   p.op = op;
   p.cmax = c->cmax;
   p.scale = 1.0f / (float)c->P;  // fl32(1/P)
@@ -433,7 +440,7 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
   p.timeout_ns = c->timeout_ns;
   p.err = c->err;
   p.trace = c->trace;
-  p.stream_every = (int)(env_size("DDL_STREAM_EVERY", 1) ? env_size("DDL_STREAM_EVERY", 1) : 1);
+  p.stream_every = c->stream_every;
   for (int r = 0; r < c->P; ++r) p.flags[r] = c->flags_of(r);
   return p;
 }
@@ -456,7 +463,7 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
   blocks_per_sm(fn, smem);  // sets the dynamic shared-memory attribute once
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void* args[] = {const_cast<KParams*>(&p)};
-  if (std::getenv("DDL_DEBUG"))
+  if (c->debug)
     std::fprintf(stderr, "[ddl] %s n=%llu q=%llu slice=%llu ctas=%d path=%d mode=%d P=%d loopback=%d\n",
                  pl.ll ? "ll" : pl.oneshot ? "oneshot" : "hier", (unsigned long long)p.n, (unsigned long long)p.q,
                  (unsigned long long)p.slice, pl.nctas, pl.path, p.mode, c->P, (int)c->loopback);
@@ -1169,7 +1176,8 @@ ddl_result_t ddl_local_reduce(const void* const* ins, int g, void* out, size_t c
   DDL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   // large aligned reductions (>= 32 MiB out) stream through the TMA ring: +2-6% at 64-256 MiB,
   // slower below (scripts/k5_bench.py); DDL_LR_NO_TMA=1 forces the register path
-  if (vec && count * elem_size(dt) >= (32u << 20) && env_size("DDL_LR_NO_TMA", 0) == 0) {
+  static const bool lr_tma = env_size("DDL_LR_NO_TMA", 0) == 0;
+  if (vec && count * elem_size(dt) >= (32u << 20) && lr_tma) {
     const void* tfn = dt == DDL_INT32 ? (const void*)ddl_local_reduce_tma_kernel<int32_t>
                       : dt == DDL_FLOAT32 ? (const void*)ddl_local_reduce_tma_kernel<float>
                                           : (const void*)ddl_local_reduce_tma_kernel<__nv_bfloat16>;

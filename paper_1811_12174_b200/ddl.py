@@ -175,18 +175,23 @@ def _torch():
     return torch
 
 
+_DTYPE_NAMES = {}
+
+
 def dtype_name(t) -> str:
-    torch = _torch()
-    m = {torch.int32: "int32", torch.float32: "float32", torch.bfloat16: "bfloat16"}
-    if t.dtype not in m:
+    if not _DTYPE_NAMES:
+        torch = _torch()
+        _DTYPE_NAMES.update({torch.int32: "int32", torch.float32: "float32", torch.bfloat16: "bfloat16"})
+    name = _DTYPE_NAMES.get(t.dtype)
+    if name is None:
         raise DDLError(ERR_UNSUPPORTED, f"dtype {t.dtype}")
-    return m[t.dtype]
+    return name
 
 
 def _stream(stream=None) -> int:
-    torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    return _torch().cuda.current_stream().cuda_stream
 
 
 def _require_cuda(t) -> None:
