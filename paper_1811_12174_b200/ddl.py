@@ -188,10 +188,21 @@ def dtype_name(t) -> str:
     return name
 
 
-def _stream(stream=None) -> int:
+_RAW_STREAM = []
+
+
+def _stream(stream=None, device=None) -> int:
+    """cudaStream_t of `stream`, else of the current stream of `device` (default: current
+    device).  torch.cuda.current_stream() costs ~3 us per call; the raw-handle query ~0.2."""
     if stream is not None:
         return stream.cuda_stream
-    return _torch().cuda.current_stream().cuda_stream
+    torch = _torch()
+    if not _RAW_STREAM:
+        _RAW_STREAM.append(getattr(torch._C, "_cuda_getCurrentRawStream", None))
+    raw = _RAW_STREAM[0]
+    if raw is None:
+        return torch.cuda.current_stream(device).cuda_stream
+    return raw(torch.cuda.current_device() if device is None else device)
 
 
 def _require_cuda(t) -> None:
@@ -264,14 +275,14 @@ class Comm:
         inside = self.buffer_ptr <= t.data_ptr() and t.data_ptr() + nbytes <= self.buffer_ptr + self.buffer_bytes
         piece = (self.buffer_bytes // t.element_size()) // 256 * 256
         if inside or nbytes <= self.buffer_bytes or piece == 0:
-            _check(_lib.ddl_allreduce(self.h, t.data_ptr(), t.numel(), dt, OP_CODES[op], _stream(stream)),
-                   "ddl_allreduce")
+            _check(_lib.ddl_allreduce(self.h, t.data_ptr(), t.numel(), dt, OP_CODES[op],
+                                      _stream(stream, t.device.index)), "ddl_allreduce")
             return t
         flat = t.view(-1)
         for lo in range(0, t.numel(), piece):
             part = flat[lo:lo + piece]
-            _check(_lib.ddl_allreduce(self.h, part.data_ptr(), part.numel(), dt, OP_CODES[op], _stream(stream)),
-                   "ddl_allreduce")
+            _check(_lib.ddl_allreduce(self.h, part.data_ptr(), part.numel(), dt, OP_CODES[op],
+                                      _stream(stream, t.device.index)), "ddl_allreduce")
         return t
 
     def register(self, t) -> int:
@@ -298,7 +309,8 @@ class Comm:
         if inp.numel() != out.numel() * self.nranks or inp.dtype != out.dtype:
             raise DDLError(ERR_INVALID_ARGUMENT, "reduce_scatter: inp must hold nranks * out.numel()")
         _check(_lib.ddl_reduce_scatter(self.h, inp.data_ptr(), out.data_ptr(), out.numel(),
-                                       DTYPE_CODES[dtype_name(out)], OP_CODES[op], _stream(stream)),
+                                       DTYPE_CODES[dtype_name(out)], OP_CODES[op],
+                                       _stream(stream, out.device.index)),
                "ddl_reduce_scatter")
         return out
 
@@ -308,7 +320,7 @@ class Comm:
         if out.numel() != inp.numel() * self.nranks or inp.dtype != out.dtype:
             raise DDLError(ERR_INVALID_ARGUMENT, "all_gather: out must hold nranks * inp.numel()")
         _check(_lib.ddl_allgather(self.h, inp.data_ptr(), out.data_ptr(), inp.numel(),
-                                  DTYPE_CODES[dtype_name(out)], _stream(stream)), "ddl_allgather")
+                                  DTYPE_CODES[dtype_name(out)], _stream(stream, out.device.index)), "ddl_allgather")
         return out
 
     def set_algo(self, algo: int, oneshot_max_bytes: int = 512 << 10) -> None:
@@ -387,21 +399,23 @@ class Loopback:
         for b in bufs:
             _require_cuda(b)
         _check(_lib.ddl_group_allreduce(self.h, _ptrs([b.data_ptr() for b in bufs]), bufs[0].numel(),
-                                        DTYPE_CODES[dtype_name(bufs[0])], OP_CODES[op], _stream(stream)),
+                                        DTYPE_CODES[dtype_name(bufs[0])], OP_CODES[op],
+                                        _stream(stream, bufs[0].device.index)),
                "ddl_group_allreduce")
         return bufs
 
     def reduce_scatter(self, outs, inps, op: str = "sum", stream=None):
         _check(_lib.ddl_group_reduce_scatter(self.h, _ptrs([t.data_ptr() for t in inps]),
                                              _ptrs([t.data_ptr() for t in outs]), outs[0].numel(),
-                                             DTYPE_CODES[dtype_name(outs[0])], OP_CODES[op], _stream(stream)),
+                                             DTYPE_CODES[dtype_name(outs[0])], OP_CODES[op],
+                                             _stream(stream, outs[0].device.index)),
                "ddl_group_reduce_scatter")
         return outs
 
     def all_gather(self, outs, inps, stream=None):
         _check(_lib.ddl_group_allgather(self.h, _ptrs([t.data_ptr() for t in inps]),
                                         _ptrs([t.data_ptr() for t in outs]), inps[0].numel(),
-                                        DTYPE_CODES[dtype_name(outs[0])], _stream(stream)),
+                                        DTYPE_CODES[dtype_name(outs[0])], _stream(stream, outs[0].device.index)),
                "ddl_group_allgather")
         return outs
 
@@ -536,10 +550,20 @@ class InProcessGroup:
 
 # ---------------------------------------------------------------- K5
 def local_reduce(ins, out, scale: float = 1.0, stream=None):
-    """out = scale * sum_j ins[j] (ascending j), the 1-GPU HBM-roofline kernel."""
+    """out = scale * sum_j ins[j] (ascending j), the 1-GPU HBM-roofline kernel (launched on
+    out's device)."""
     for t in list(ins) + [out]:
         _require_cuda(t)
-    _check(_lib.ddl_local_reduce(_ptrs([t.data_ptr() for t in ins]), len(ins), out.data_ptr(), out.numel(),
-                                 DTYPE_CODES[dtype_name(out)], float(scale), _stream(stream)),
-           "ddl_local_reduce")
+    torch = _torch()
+    dev = out.device.index
+
+    def call():
+        _check(_lib.ddl_local_reduce(_ptrs([t.data_ptr() for t in ins]), len(ins), out.data_ptr(), out.numel(),
+                                     DTYPE_CODES[dtype_name(out)], float(scale), _stream(stream, dev)),
+               "ddl_local_reduce")
+    if dev == torch.cuda.current_device():
+        call()
+    else:
+        with torch.cuda.device(dev):
+            call()
     return out
