@@ -10,7 +10,8 @@ integer-valued inputs equal to the closed form P*(P+1)/2 (no oracle on this path
 Timing: CUDA-graph replay of `iters` calls (device time, no host launch cost), CUDA events,
 max over ranks.  Columns: impl,P,dims,dtype,op,bytes,us,algbw_GBs,busbw_GBs,pct_roof,roof
 (roof = HBM copy peak for loopback rows -- against the schedule's algorithmic HBM bytes --
-and 900 GB/s NVLink for N > 1).
+and 900 GB/s NVLink for N > 1).  The P = 1 rows of config 5 are the K5 local reduce (g = 8
+buffers of S bytes -> 1): algbw column = (g+1)*S / t against the HBM peak.
 """
 import argparse
 import math
@@ -48,9 +49,12 @@ def time_graph(fn, iters):
 
 def rows_for(config):
     """(P, dims_spec, dtype, op, bytes) per row at loopback P = 8 (or N)."""
-    if config == "sweep":         # config 5: fp32 1 KiB .. 1 GiB, sum
+    if config == "sweep":         # config 5: fp32 1 KiB .. 1 GiB, sum, at P = 1 / 2 / 4 / 8
         sizes = [1024 << j for j in range(21)]
-        return [(None, d, "float32", "sum", s) for d in (None, "2x4", "2x2x2") for s in sizes]
+        rows = [(None, d, "float32", "sum", s) for d in (None, "2x4", "2x2x2") for s in sizes]
+        rows += [(P, str(P), "float32", "sum", s) for P in (2, 4) for s in sizes]   # loopback only
+        rows += [(1, "k5", "float32", "sum", s) for s in sizes]   # P = 1: the K5 local reduce, g = 8
+        return rows
     if config == "bf16":          # config 4: bf16 256 MiB, avg, 8 vs 2x4 vs 2x2x2 (and 4x2)
         return [(8, d, "bfloat16", "avg", 256 << 20) for d in ("8", "2x4", "2x2x2", "4x2")]
     if config == "unet3d":        # config 3: 19,075,523 fp32, avg, 2/4/8 ranks, 2x2x2-style dims
@@ -58,20 +62,39 @@ def rows_for(config):
     raise SystemExit(f"unknown config {config}")
 
 
+def k5_row(S, dtype, hbm, out, g=8):
+    """P = 1 row of the sweep: out = sum of g local buffers of S bytes (K5), against HBM."""
+    w = torch.tensor([], dtype=TD[dtype]).element_size()
+    n = S // w
+    ins = [torch.full((n,), j + 1, dtype=TD[dtype], device="cuda") for j in range(g)]
+    out_t = torch.empty(n, dtype=TD[dtype], device="cuda")
+    ddl.local_reduce(ins, out_t)
+    torch.cuda.synchronize()
+    assert bool((out_t == g * (g + 1) // 2).all()), ("k5", S)
+    iters = max(3, min(200, int(2e9 // max(S * (g + 1), 1))))
+    us = time_graph(lambda: ddl.local_reduce(ins, out_t), iters)
+    hb = (g + 1) * S
+    print(",".join(map(str, ["ddl-local-reduce-g8", 1, "-", dtype, "sum", S, f"{us:.2f}", f"{hb / us / 1e3:.2f}", "-",
+                             f"{hb / us / 1e3 / hbm * 100:.1f}", "hbm"])), file=out, flush=True)
+
+
 def loopback(args, out):
     hbm, _ = bench.peaks()
     cache = {}
     for P, spec, dtype, op, S in rows_for(args.config):
+        if spec == "k5":
+            k5_row(S, dtype, hbm, out)
+            continue
         P = P or 8
         spec = spec or str(P)
         dims = ddl.parse_dims(spec)
-        if (P, spec) not in cache:
-            cache[(P, spec)] = ddl.Loopback(P, dims)
-        lb = cache[(P, spec)]
         w = torch.tensor([], dtype=TD[dtype]).element_size()
         n = S // w
         if P * S > args.max_total_bytes:
             continue
+        if (P, spec) not in cache:
+            cache[(P, spec)] = ddl.Loopback(P, dims)
+        lb = cache[(P, spec)]
         bufs = [torch.full((n,), r + 1, dtype=TD[dtype], device="cuda") for r in range(P)]
         lb.all_reduce(bufs, "sum")
         torch.cuda.synchronize()
@@ -98,7 +121,7 @@ def multi(args, out):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comms = {}
     for P, spec, dtype, op, S in rows_for(args.config):
-        if P not in (None, world):
+        if P not in (None, world) or spec == "k5":
             continue
         spec = spec or str(world)
         if math.prod(ddl.parse_dims(spec)) != world:
