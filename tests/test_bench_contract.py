@@ -1,0 +1,67 @@
+"""bench.py's driver contract on CPU: `--impl reference` (the oracle arm, no GPU) prints ONE
+JSON line with the required keys and sane values, and the pure helpers bench.py computes
+its roofline from agree with the planner (algorithmic HBM bytes of the loopback schedule)."""
+import json
+import os
+import subprocess
+import sys
+
+import bench
+from paper_1811_12174_b200 import ddl
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REQUIRED = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+            "scaling", "vs_baseline", "dtype", "data", "config")
+
+
+def test_reference_arm_json_line():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    for k in REQUIRED:
+        assert k in d, k
+    assert d["impl"] == "reference"
+    assert d["metric"] == json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+    assert d["steps"] == 1 and d["warmup"] == 3 and d["n_gpus"] == 1
+    assert d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert "workload" in d["config"]
+
+
+def test_reference_arm_other_ranks_exit_quietly():
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+                       env=env)
+    assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_loopback_algorithmic_bytes_match_planner_traffic():
+    """bench.loopback_hbm_bytes (roofline numerator) = per rank: own reads + writes of every
+    phase, which for the RS reads is (peer bytes from ddl_plan_traffic) + own block bytes;
+    checked against an independent count from the planner's block sets."""
+    P, w = 8, 4
+    for dims in ([4, 2], [8], [2, 2, 2], [2, 4]):
+        for n in (1 << 20, 1_000_003, 2049000):
+            got = bench.loopback_hbm_bytes(n, P, dims, w)
+            q = ddl.block_elems(n, P, "float32")
+
+            def blen(b):
+                return max(0, min(n, (b + 1) * q) - min(n, b * q)) * w
+            want = 0
+            for r in range(P):
+                for d in range(len(dims)):
+                    if dims[d] == 1:
+                        continue
+                    act = ddl.plan_blocks(P, dims, r, d + 1)   # blocks r reduces in RS d / receives in AG d
+                    byts = sum(blen(b) for b in act)
+                    want += dims[d] * byts + byts              # RS d: read g copies, write one
+                    for m in ddl.plan_group(P, dims, r, d):    # AG d: read + write every peer's set
+                        if m != r:
+                            mb = sum(blen(b) for b in ddl.plan_blocks(P, dims, m, d + 1))
+                            want += 2 * mb
+            assert got == want, (dims, n, got, want)
