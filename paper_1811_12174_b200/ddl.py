@@ -362,11 +362,21 @@ def auto_dims(world: int, local_world: int | None = None) -> list[int]:
 
 def init(dims=None, group=None, max_bytes: int = 256 << 20) -> Comm:
     """``ddl.init(dims)``: the analogue of the paper's ``import ddl`` + ``ddlrun`` setup
-     under torchrun.  ``dims="auto"`` picks :func:`auto_dims`."""
+     under torchrun.  ``dims="auto"`` picks :func:`auto_dims`.  The
+    environment variable ``DDL_DIMS`` (e.g. ``2x4``, or ``auto``) overrides ``dims`` -- the
+    role of ddlrun's topology configuration -- and must be equal on every rank."""
+    import torch.distributed as dist
+    return Comm(resolve_dims(dims, dist.get_world_size(group)), group, max_bytes)
+
+
+def resolve_dims(dims, world: int, local_world: int | None = None) -> list[int]:
+    """dims as ddl.init takes them, after the DDL_DIMS override: None -> [world], "auto" ->
+    auto_dims, "2x4" -> [4, 2], a list as is (innermost first)."""
+    import os
+    dims = os.environ.get("DDL_DIMS") or dims
     if isinstance(dims, str) and dims == "auto":
-        import torch.distributed as dist
-        dims = auto_dims(dist.get_world_size(group))
-    return Comm(dims, group, max_bytes)
+        return auto_dims(world, local_world)
+    return parse_dims(dims, world)
 
 
 def _tensor_from_ptr(ptr: int, nbytes: int, device: int):

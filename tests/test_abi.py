@@ -210,6 +210,18 @@ def test_plain_c_client(tmp_path):
     assert "c_abi_smoke ok" in r.stdout
 
 
+def test_resolve_dims_and_env_override(monkeypatch):
+    monkeypatch.delenv("DDL_DIMS", raising=False)
+    assert ddl.resolve_dims(None, 8) == [8]
+    assert ddl.resolve_dims("2x4", 8) == [4, 2]
+    assert ddl.resolve_dims([2, 2, 2], 8) == [2, 2, 2]
+    assert ddl.resolve_dims("auto", 8, 4) == [4, 2]
+    monkeypatch.setenv("DDL_DIMS", "2x2x2")          # ddlrun-style override
+    assert ddl.resolve_dims("2x4", 8) == [2, 2, 2]
+    monkeypatch.setenv("DDL_DIMS", "auto")
+    assert ddl.resolve_dims(None, 16, 8) == [8, 2]
+
+
 def test_auto_dims():
     assert ddl.auto_dims(8, 8) == [8]            # one NVSwitch node: flat
     assert ddl.auto_dims(8, 4) == [4, 2]         # "2x4": 2 nodes x 4 GPUs

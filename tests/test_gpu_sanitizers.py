@@ -1,4 +1,4 @@
-"""compute-sanitizer tiers: memcheck and racecheck over every kernel
+"""compute-sanitizer tiers: memcheck, racecheck, synccheck and initcheck over every kernel
 variant on tiny ragged inputs (scripts/sanitize_check.py) report zero errors."""
 import os
 import shutil
@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_sanitizer_clean(tool):
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(cs):
