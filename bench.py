@@ -327,7 +327,11 @@ def run_loopback(args):
                      "peak_source": peak_src,
                      "kernel": "ddl_hier_kernel<float,2> (TMA-staged; loopback, all 8 virtual ranks in one launch)",
                      "algorithmic_bytes_per_step": algo_bytes // args.steps,
-                     "kernel_ms_per_step": kern_ms / args.steps},
+                     "kernel_ms_per_step": kern_ms / args.steps,
+                     # physical view: profiled DRAM bytes of a step / this run's kernel time
+                     "dram_frac": ((tr2 / (kern_ms / args.steps * 1e-3) / 1e9 / hbm_peak)
+                                   if (tr2 := profiled_traffic("resnet50-grad-set 8 virtual ranks dims 2x4 avg"))
+                                   and dims == [4, 2] else None)},
         "e2e": {"value": S_total * 2 * (P - 1) / P / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": S_total * P, "d2h_bytes_per_step": S_total},
         "gpu_launches": nb * args.steps,
