@@ -23,13 +23,18 @@ def ddl_allreduce_hook(state: Comm, bucket: dist.GradBucket) -> torch.futures.Fu
     stream, so DDP's copy-back is stream-ordered after it).  Each bucket buffer is
     registered with DDL the first time it is seen (a collective every rank performs at the
     same bucket), so every later step all-reduces it zero-copy instead of staging it
-    through the workspace.  DDP's buffers are persistent (they change only if DDP rebuilds
-    its buckets, which then registers the new ones)."""
+    through the workspace.  DDP's buffers are persistent; they change only when DDP rebuilds
+    its buckets (after the first iteration), and then the bucket's previous registration is
+    dropped before the new buffer is registered -- a stale registration would make a later
+    tensor allocated at the old address look zero-copy and read the peers' old buffers."""
     buf = bucket.buffer()
-    regs = state.__dict__.setdefault("_ddp_registered", {})
+    regs = state.__dict__.setdefault("_ddp_registered", {})   # bucket index -> (key, reg_id)
     key = (buf.data_ptr(), buf.numel() * buf.element_size())
-    if key not in regs:
-        regs[key] = state.register(buf)
+    have = regs.get(bucket.index())
+    if have is None or have[0] != key:
+        if have is not None:
+            state.deregister(have[1])
+        regs[bucket.index()] = (key, state.register(buf))
     state.all_reduce(buf, "avg")
     fut = torch.futures.Future()
     fut.set_result(buf)

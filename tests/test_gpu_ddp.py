@@ -57,7 +57,23 @@ def _rank_main(rank, world, port, q):
             opt.step()
         torch.cuda.synchronize()
         params = [p.detach().cpu().numpy() for p in model.module.parameters()]  # by value
-        q.put((rank, params, comm.async_error()))
+        nreg = len(comm._ddp_registered)
+        # a rebuilt bucket (same index, new buffer): the old registration is dropped, the new
+        # buffer registered and reduced zero-copy -- the registration count does not grow
+        class _Bucket:
+            def __init__(self, t, i):
+                self.t, self.i = t, i
+
+            def buffer(self):
+                return self.t
+
+            def index(self):
+                return self.i
+        nb = torch.full((5000,), float(rank + 1), device="cuda")
+        ddl_allreduce_hook(comm, _Bucket(nb, 0)).wait()
+        torch.cuda.synchronize()
+        rebuilt_ok = bool((nb == (world + 1) / 2).all()) and len(comm._ddp_registered) == nreg
+        q.put((rank, params, comm.async_error() if rebuilt_ok else -2))
         comm.finalize()
     except Exception as e:
         q.put((rank, repr(e), -1))
