@@ -66,6 +66,7 @@ struct KParams {
   const void* cin[kMaxRanks];   // copy-in source of each rank
   void* cout[kMaxRanks];        // copy-out destination of each rank
   int mode;
+  int nwaves;          // hier: slices per CTA, run one after another (wave w = slice w*gridDim.x + blockIdx.x)
   uint64_t* trace;     // debug (DDL_TRACE=1): [P][cmax][kTraceEvents] globaltimer stamps, else null
   int stream_every;    // PATH 5: publish progress every k chunks (and at the phase end)
   uint32_t sig;        // DDL_CHECK=1: signature of (count, dtype, op, algorithm); 0 = no check
@@ -325,9 +326,9 @@ struct Span {
 };
 
 template <int W>
-__device__ __forceinline__ Span slice_span(const KParams& p, int b) {
+__device__ __forceinline__ Span slice_span(const KParams& p, int b, int sidx) {
   Span s{0, 0, 0};
-  const uint64_t cbase = (uint64_t)blockIdx.x * p.slice;
+  const uint64_t cbase = (uint64_t)sidx * p.slice;
   if (cbase >= p.q) return s;
   const uint64_t e0 = (uint64_t)b * p.q + cbase;
   if (e0 >= p.n) return s;
@@ -349,6 +350,7 @@ enum PhaseKind : int { kPhRS = 0, kPhAG = 1, kPhCin = 2, kPhCinOwn = 3, kPhCout 
 
 struct PhaseCtx {
   int kind, d, g, nunits, nb, c;
+  int s;  // slice index this CTA handles in this phase (blockIdx.x, or w*gridDim.x + blockIdx.x)
   bool first, last;
 };
 
@@ -362,6 +364,7 @@ __device__ __forceinline__ PhaseCtx phase_ctx(const KParams& p, int me, int kind
   x.c = 0;
   x.nb = 0;
   x.g = 1;
+  x.s = blockIdx.x;
   if (kind == kPhRS) {
     x.g = t.g[d];
     x.nb = nblocks(t, d + 1);
@@ -520,7 +523,7 @@ __device__ __forceinline__ void fill_units(const KParams& p, int me, const Phase
   __syncthreads();  // the previous phase's readers of the tables are done
   if ((int)threadIdx.x < x.nunits) {
     int sr;
-    const Span sp = slice_span<W>(p, unit_block(p, me, x, threadIdx.x, &sr));
+    const Span sp = slice_span<W>(p, unit_block(p, me, x, threadIdx.x, &sr), x.s);
     units[threadIdx.x] = UnitDesc{sp.e0, sp.nvec * (uint32_t)(W * sizeof(T)), sp.rem,
                                   x.kind == kPhRS ? nullptr : src_base<T>(p, me, x, 0, sr)};
   }
@@ -808,55 +811,77 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
     return true;
   };
   // trace events: 0 start, 1 after copy-in, 2+2j after barrier j, 3+2j after the phase it gates,
-  // 2+2*(2L) after the end barrier
+  // 2+2*(2L) after the end barrier (waves > 1: the last wave's)
   trace_ev(p, me, 0);
-  if (p.mode & kCinAll) run(phase_ctx(p, me, kPhCin, 0, false, false), -1);
-  if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T))
-    run(phase_ctx(p, me, kPhCinOwn, 0, false, false), -1);
-  trace_ev(p, me, 1);
   // Loopback: every virtual rank's inputs are ready when the launch starts and nothing can
   // touch any buffer before the whole launch ends (stream order), so the start barrier
   // (when there is no copy-in) and the end barrier are implied by the kernel boundary.
-  const bool implied_start = p.loopback && !(p.mode & (kCinAll | kCinOwn));
-  if (p.mode & kRS) {
-    for (int j = 0; j < L; ++j) {
-      if (!settle(j)) return;
-      if (!(j == 0 && implied_start) && !(STREAM && j > 0) &&
-          !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j), j == 0))
-        return;
-      trace_ev(p, me, 2 + 2 * j);
-      prev = phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1);
-      run(prev, j);
-      have_prev = true;
-      trace_ev(p, me, 3 + 2 * j);
+  const bool cin = (p.mode & (kCinAll | kCinOwn)) != 0;
+  const bool implied_start = p.loopback && !cin;
+  // Waves: the call is nwaves independent all-reduces of disjoint element sets (slice
+  // w*gridDim.x + blockIdx.x of every block), run one after another by each CTA, so the
+  // working set of a wave can stay in L2 and one CTA's barrier waits overlap other CTAs'
+  // streaming.  Wave w's barriers release epoch e+w (the rank epoch advances by nwaves per
+  // call; flags are monotone, so a peer already in a later wave also satisfies the wait).
+  // Without copy-in the inputs of every wave are ready at the call start (barrier 0 of wave 0
+  // covers them) and no wave writes what another wave reads, so barrier 0 of waves > 0 is
+  // skipped; with copy-in it publishes that wave's copied slice.
+  const int nw = p.nwaves > 1 ? p.nwaves : 1;
+  uint32_t ew = e;
+  for (int w = 0; w < nw; ++w) {
+    ew = e + (uint32_t)w;
+    const int sidx = w * (int)gridDim.x + (int)blockIdx.x;
+    const bool tr = w == nw - 1;
+    auto ctx = [&](int kind, int d, bool first, bool last) {
+      PhaseCtx x = phase_ctx(p, me, kind, d, first, last);
+      x.s = sidx;
+      return x;
+    };
+    if (p.mode & kCinAll) run(ctx(kPhCin, 0, false, false), -1);
+    if ((p.mode & kCinOwn) && p.cin[me] != static_cast<const char*>(p.work[me]) + (size_t)me * p.q * sizeof(T))
+      run(ctx(kPhCinOwn, 0, false, false), -1);
+    if (tr) trace_ev(p, me, 1);
+    const bool skip_b0 = (w == 0 && implied_start) || (w > 0 && !cin);
+    if (p.mode & kRS) {
+      for (int j = 0; j < L; ++j) {
+        if (!settle(j)) return;
+        if (!(j == 0 && skip_b0) && !(STREAM && j > 0) &&
+            !dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j), j == 0 && w == 0))
+          return;
+        if (tr) trace_ev(p, me, 2 + 2 * j);
+        prev = ctx(kPhRS, t.live[j], j == 0, j == L - 1);
+        run(prev, j);
+        have_prev = true;
+        if (tr) trace_ev(p, me, 3 + 2 * j);
+      }
     }
-  }
-  if (p.mode & kAG) {
-    for (int jj = 0; jj < L; ++jj) {
-      const int j = L + jj;
-      if (!settle(j)) return;
-      if (!(STREAM && (p.mode & kRS)) &&
-          !dbarrier(p, me, j, barrier_npeers(t, j), e, group_peer(j), jj == 0 && !(p.mode & kRS)))
-        return;
-      trace_ev(p, me, 2 + 2 * j);
-      prev = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false);
-      run(prev, j);
-      have_prev = true;
-      trace_ev(p, me, 3 + 2 * j);
+    if (p.mode & kAG) {
+      for (int jj = 0; jj < L; ++jj) {
+        const int j = L + jj;
+        if (!settle(j)) return;
+        if (!(STREAM && (p.mode & kRS)) && !((p.mode & kRS) == 0 && jj == 0 && w > 0 && !cin) &&
+            !dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j), jj == 0 && !(p.mode & kRS) && w == 0))
+          return;
+        if (tr) trace_ev(p, me, 2 + 2 * j);
+        prev = ctx(kPhAG, t.live[L - 1 - jj], false, false);
+        run(prev, j);
+        have_prev = true;
+        if (tr) trace_ev(p, me, 3 + 2 * j);
+      }
     }
-  }
-  const int last_phase = (p.mode & kAG) ? 2 * L - 1 : L - 1;
-  if (p.mode & kCoutAll) {
-    if (!settle(last_phase + 1)) return;
-    __syncthreads();
-    run(phase_ctx(p, me, kPhCout, 0, false, false), -1);
-  }
-  if (L > 0 && !p.loopback) {
-    if (!(p.mode & kCoutAll) && !settle(last_phase + 1)) return;
-    if (!dbarrier(p, me, 2 * L, barrier_npeers(t, 2 * L), e, group_peer(2 * L))) return;
+    const int last_phase = (p.mode & kAG) ? 2 * L - 1 : L - 1;
+    if (p.mode & kCoutAll) {
+      if (!settle(last_phase + 1)) return;
+      __syncthreads();
+      run(ctx(kPhCout, 0, false, false), -1);
+    }
+    if (w == nw - 1 && L > 0 && !p.loopback) {
+      if (!(p.mode & kCoutAll) && !settle(last_phase + 1)) return;
+      if (!dbarrier(p, me, 2 * L, barrier_npeers(t, 2 * L), ew, group_peer(2 * L))) return;
+    }
   }
   trace_ev(p, me, 2 + 2 * (2 * L));
-  rank_epoch_end(p, me, e, STEAL ? 2 * L : 0);
+  rank_epoch_end(p, me, ew, STEAL ? 2 * L : 0);
 }
 
 // ------------------------------------------------------------------------ one-shot (a9)

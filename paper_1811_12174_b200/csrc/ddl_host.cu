@@ -3,6 +3,7 @@
 // launches.  See DESIGN.md for the design and the paper citations.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -145,6 +146,9 @@ struct ddl_comm {
   int gpu_share = 1;        // ranks sharing this GPU (loopback: P; in-process test groups: P)
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
+  int waves = 0;                           // DDL_WAVES: slices per CTA per hierarchical call (0 = auto)
+  size_t wave_slice_bytes = 112 << 10;     // auto: target per-CTA slice of one wave
+  size_t min_wave_slice_bytes = 16 << 10;  // no waves below this slice size
   bool use_pdl = true;  // programmatic dependent launch (DDL_PDL=0: plain stream order)
   bool force_sys = false;  // DDL_FORCE_SYS_SCOPE=1: .sys flags even when every rank shares this GPU
   bool debug = false;      // DDL_DEBUG: one stderr line per launch
@@ -242,6 +246,11 @@ void apply_env(ddl_comm* c) {
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   c->ll_max = env_size("DDL_LL_MAX_BYTES", c->ll_max);
   c->use_pdl = env_size("DDL_PDL", 1) != 0;
+  c->waves = (int)env_size("DDL_WAVES", c->waves);
+  if (c->waves > 64) c->waves = 64;
+  c->wave_slice_bytes = env_size("DDL_WAVE_SLICE_BYTES", c->wave_slice_bytes);
+  if (c->wave_slice_bytes < 4096) c->wave_slice_bytes = 4096;
+  c->min_wave_slice_bytes = env_size("DDL_MIN_WAVE_SLICE_BYTES", c->min_wave_slice_bytes);
   c->force_sys = env_size("DDL_FORCE_SYS_SCOPE", 0) != 0;
   c->debug = std::getenv("DDL_DEBUG") != nullptr;
   c->stream_every = (int)env_size("DDL_STREAM_EVERY", 1);
@@ -290,6 +299,7 @@ struct Plan {
   bool oneshot = false;
   bool ll = false;  // LL one-shot (multi-process small messages)
   int r = 1;        // one-shot: vectors per thread
+  int nwaves = 1;   // hierarchical: slices per CTA, run as successive waves
 };
 
 template <typename T>
@@ -372,6 +382,24 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
   pl.slice = slice;
   pl.nctas = (int)((q + slice - 1) / slice);
   if (pl.nctas < 1) pl.nctas = 1;
+  // Waves (PATH 1/2 only): the same CTAs walk nwaves slices each, one wave after another.
+  // Auto (DDL_WAVES unset): about one wave per wave_slice_bytes of per-CTA slice, at most 32,
+  // when every rank is on this GPU (loopback / in-process: measured 6-17 % faster from 64 MiB
+  // up, slower below, profiles/r01_waves_sweep.txt); across GPUs one wave until the barrier
+  // cost over NVLink is measured.  DDL_WAVES=k forces k.
+  int waves = c->waves;
+  if (waves == 0) {
+    const uint64_t sb = pl.slice * (uint64_t)w;
+    waves = (c->gpu_share == c->P) ? (int)std::min<uint64_t>(32, sb / c->wave_slice_bytes) : 1;
+  }
+  if (waves > 1 && pl.path <= 2) {
+    uint64_t s2 = (q + (uint64_t)pl.nctas * waves - 1) / ((uint64_t)pl.nctas * waves);
+    s2 = (s2 + W - 1) / W * W;
+    if (s2 * w >= c->min_wave_slice_bytes) {
+      pl.slice = s2;
+      pl.nwaves = (int)((q + (uint64_t)pl.nctas * s2 - 1) / ((uint64_t)pl.nctas * s2));
+    }
+  }
   (void)n;
   return pl;
 }
@@ -450,7 +478,7 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
   if (c->check && !c->loopback) {  // FNV-1a over what every rank must agree on
     uint32_t h = 2166136261u;
     const uint64_t vals[] = {p.n, (uint64_t)dt, (uint64_t)p.op, (uint64_t)p.mode, (uint64_t)pl.oneshot,
-                             (uint64_t)pl.path, (uint64_t)pl.nctas, p.q, (uint64_t)pl.ll};
+                             (uint64_t)pl.path, (uint64_t)pl.nctas, p.q, (uint64_t)pl.ll, (uint64_t)pl.nwaves};
     for (uint64_t v : vals)
       for (int b = 0; b < 8; ++b) h = (h ^ (uint32_t)((v >> (8 * b)) & 0xFF)) * 16777619u;
     p.sig = h | 1u;
@@ -459,14 +487,15 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
                    : pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive, pl.r)
                                 : hier_fn_dt(dt, pl.path);
   if (!fn) return DDL_ERR_UNSUPPORTED;
+  p.nwaves = (pl.oneshot || pl.ll) ? 1 : pl.nwaves;
   const size_t smem = (pl.oneshot || pl.ll) ? 0 : hier_smem(pl.path);
   blocks_per_sm(fn, smem);  // sets the dynamic shared-memory attribute once
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void* args[] = {const_cast<KParams*>(&p)};
   if (c->debug)
-    std::fprintf(stderr, "[ddl] %s n=%llu q=%llu slice=%llu ctas=%d path=%d mode=%d P=%d loopback=%d\n",
+    std::fprintf(stderr, "[ddl] %s n=%llu q=%llu slice=%llu ctas=%d waves=%d path=%d mode=%d P=%d loopback=%d\n",
                  pl.ll ? "ll" : pl.oneshot ? "oneshot" : "hier", (unsigned long long)p.n, (unsigned long long)p.q,
-                 (unsigned long long)p.slice, pl.nctas, pl.path, p.mode, c->P, (int)c->loopback);
+                 (unsigned long long)p.slice, pl.nctas, p.nwaves, pl.path, p.mode, c->P, (int)c->loopback);
   if (c->loopback) {
     DDL_CUDA(launch_ex(fn, dim3(pl.nctas, c->P), smem, s, args, true, c->use_pdl));
   } else {

@@ -57,7 +57,8 @@ def group(P, dims, env=None):
 VARIANTS = {"default": None, "tma": {"DDL_TMA_MIN_SLICE_BYTES": "0"},
             "stream": {"DDL_STREAM": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"},
             "steal": {"DDL_STEAL": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"},
-            "check": {"DDL_CHECK": "1"}}
+            "check": {"DDL_CHECK": "1"},
+            "waves": {"DDL_WAVES": "3", "DDL_MIN_WAVE_SLICE_BYTES": "0", "DDL_TMA_MIN_SLICE_BYTES": "0"}}
 
 
 CASES = [(2, [2]), (4, [2, 2]), (4, [4]), (8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (6, [3, 2])]
@@ -120,10 +121,13 @@ def test_reduce_scatter_allgather_staged(P, dims, variant):
     assert g.async_error() == ddl.SUCCESS
 
 
-def test_many_calls_mixed_paths():
-    """Epoch bookkeeping across calls that alternate algorithm, buffer kind and size."""
+@pytest.mark.parametrize("variant", ["default", "waves"])
+def test_many_calls_mixed_paths(variant):
+    """Epoch bookkeeping across calls that alternate algorithm, buffer kind and size (waves:
+    hierarchical calls advance the rank epoch by their wave count, interleaved with LL and
+    one-shot calls whose scratch halves follow the epoch's parity)."""
     P, dims = 4, [2, 2]
-    g = group(P, dims)
+    g = group(P, dims, VARIANTS[variant])
     g.set_algo(ddl.ALGO_AUTO, 64 << 10)
     rng = np.random.Generator(np.random.PCG64(11))
     for i in range(30):

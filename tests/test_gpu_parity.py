@@ -261,26 +261,30 @@ def test_int32_bitmask_256MiB_closed_form():
 
 
 # ------------------------------------------------------------------ alternative kernel paths
-PATH_ENVS = {"steal": "DDL_STEAL", "dyn": "DDL_DYN", "ldg": "DDL_NO_TMA", "tma-all": "DDL_TMA_MIN_SLICE_BYTES",
-             "stream": "DDL_STREAM"}
+PATH_ENVS = {"steal": {"DDL_STEAL": "1"}, "dyn": {"DDL_DYN": "1"}, "ldg": {"DDL_NO_TMA": "1"},
+             "tma-all": {"DDL_TMA_MIN_SLICE_BYTES": "0"}, "stream": {"DDL_STREAM": "1"},
+             # waves: every CTA walks 3 (5) slices one after another, down to tiny slices
+             "waves": {"DDL_WAVES": "3", "DDL_MIN_WAVE_SLICE_BYTES": "0"},
+             "waves-ldg": {"DDL_WAVES": "5", "DDL_MIN_WAVE_SLICE_BYTES": "0", "DDL_NO_TMA": "1"}}
 
 
 @pytest.mark.parametrize("path", sorted(PATH_ENVS))
 @pytest.mark.parametrize("P,dims", [(8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (6, [3, 2]), (4, [2, 2])])
 def test_kernel_paths_parity(path, P, dims):
     """Every hierarchical kernel variant (register-staged, TMA-staged for all sizes, work
-    stealing, rank-level dynamic) computes the same bits as the oracle."""
+    stealing, rank-level dynamic, streaming, waves) computes the same bits as the oracle."""
     import os
-    var = PATH_ENVS[path]
-    old = os.environ.get(var)
-    os.environ[var] = "0" if var == "DDL_TMA_MIN_SLICE_BYTES" else "1"
+    envs = PATH_ENVS[path]
+    old = {k: os.environ.get(k) for k in envs}
+    os.environ.update(envs)
     try:
         lb = ddl.Loopback(P, dims)
     finally:
-        if old is None:
-            os.environ.pop(var, None)
-        else:
-            os.environ[var] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     lb.set_algo(ddl.ALGO_HIER, 0)
     for dtype in ("int32", "float32", "bfloat16"):
         for n in (1, 7, 40_003, 1_000_003, 3_000_017):
