@@ -765,7 +765,8 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
 
 // ------------------------------------------------------------------------ the hierarchical kernel
 // PATH: 0 = element-wise loads (unaligned RS/AG layouts), 1 = 16-byte register-staged
-// loads, 2 = 16-byte TMA-staged (default), 4 = TMA-staged with work stealing.
+// loads, 2 = 16-byte TMA-staged (default), 4 = TMA-staged with work stealing, 5 = streaming,
+// 6 = TMA-staged in waves (large messages).
 template <typename T, int PATH>
 __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
   pdl_begin();
@@ -773,6 +774,7 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
   constexpr bool TMA = PATH >= 2;
   constexpr bool STEAL = PATH == 4;
   constexpr bool STREAM = PATH == 5;
+  constexpr bool WAVES = PATH == 6;
   const int me = p.loopback ? (int)blockIdx.y : p.rank;
   const uint32_t e = rank_epoch_begin(p, me);
   if (me == p.skip_rank) return;
@@ -826,8 +828,12 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
   // Without copy-in the inputs of every wave are ready at the call start (barrier 0 of wave 0
   // covers them) and no wave writes what another wave reads, so barrier 0 of waves > 0 is
   // skipped; with copy-in it publishes that wave's copied slice.
-  const int nw = p.nwaves > 1 ? p.nwaves : 1;
+  // (PATH 6 only: the TMA-staged kernel with the wave loop compiled in, so PATH 2's code and
+  // registers stay those of a single wave -- the loop cost PATH 2 1-4 % at 8-64 MiB and made
+  // the register-staged kernel spill at its 128-register cap)
+  const int nw = (WAVES && p.nwaves > 1) ? p.nwaves : 1;
   uint32_t ew = e;
+#pragma unroll 1
   for (int w = 0; w < nw; ++w) {
     ew = e + (uint32_t)w;
     const int sidx = w * (int)gridDim.x + (int)blockIdx.x;

@@ -304,6 +304,7 @@ struct Plan {
 
 template <typename T>
 const void* hier_fn(int path) {
+  if (path == 6) return (const void*)ddl_hier_kernel<T, 6>;
   if (path == 5) return (const void*)ddl_hier_kernel<T, 5>;
   if (path == 4) return (const void*)ddl_hier_kernel<T, 4>;
   if (path == 3) return (const void*)ddl_dyn_kernel<T>;
@@ -382,7 +383,7 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
   pl.slice = slice;
   pl.nctas = (int)((q + slice - 1) / slice);
   if (pl.nctas < 1) pl.nctas = 1;
-  // Waves (PATH 1/2 only): the same CTAs walk nwaves slices each, one wave after another.
+  // Waves (TMA-staged PATH 2 only): the same CTAs walk nwaves slices each, one wave after another.
   // Auto (DDL_WAVES unset): about one wave per wave_slice_bytes of per-CTA slice, at most 32,
   // when every rank is on this GPU (loopback / in-process: measured 6-17 % faster from 64 MiB
   // up, slower below, profiles/r01_waves_sweep.txt); across GPUs one wave until the barrier
@@ -392,12 +393,18 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
     const uint64_t sb = pl.slice * (uint64_t)w;
     waves = (c->gpu_share == c->P) ? (int)std::min<uint64_t>(32, sb / c->wave_slice_bytes) : 1;
   }
-  if (waves > 1 && pl.path <= 2) {
+  if (waves > 1 && pl.path == 2) {
     uint64_t s2 = (q + (uint64_t)pl.nctas * waves - 1) / ((uint64_t)pl.nctas * waves);
     s2 = (s2 + W - 1) / W * W;
     if (s2 * w >= c->min_wave_slice_bytes) {
       pl.slice = s2;
       pl.nwaves = (int)((q + (uint64_t)pl.nctas * s2 - 1) / ((uint64_t)pl.nctas * s2));
+      if (pl.nwaves > 1) pl.path = 6;  // the TMA-staged kernel with the wave loop compiled in
+      if (pl.path == 6 && cap_per_rank(c, hier_fn_dt(dt, 6), hier_smem(6)) < pl.nctas) {
+        pl.path = 2;  // the wave kernel would not keep every CTA resident: one wave
+        pl.nwaves = 1;
+        pl.slice = slice;
+      }
     }
   }
   (void)n;
