@@ -10,13 +10,15 @@ def check(bufs, want):
     assert all(bool((b == want).all()) for b in bufs)
 
 import os
-runs = [((4, [2, 2]), None), ((8, [4, 2]), None), ((3, [3]), None),
-        ((4, [2, 2]), "DDL_TMA_MIN_SLICE_BYTES"), ((8, [4, 2]), "DDL_TMA_MIN_SLICE_BYTES")]
+TMA = {"DDL_TMA_MIN_SLICE_BYTES": "0"}     # TMA-staged path even for these tiny slices
+WAVES = dict(TMA, DDL_WAVES="3", DDL_MIN_WAVE_SLICE_BYTES="0")   # the wave kernel (PATH 6)
+runs = [((4, [2, 2]), {}), ((8, [4, 2]), {}), ((3, [3]), {}),
+        ((4, [2, 2]), TMA), ((8, [4, 2]), TMA), ((8, [2, 2, 2]), WAVES)]
 for (P, dims), force in runs:
-    if force:
-        os.environ[force] = "0"          # TMA-staged path even for these tiny slices
+    os.environ.update(force)
     lb = ddl.Loopback(P, dims)
-    os.environ.pop("DDL_TMA_MIN_SLICE_BYTES", None)
+    for k in force:
+        os.environ.pop(k, None)
     for algo in (ddl.ALGO_HIER, ddl.ALGO_ONESHOT):
         lb.set_algo(algo, 1 << 30)
         for n in (1, 1003, 70_001):
@@ -37,22 +39,29 @@ for (P, dims), force in runs:
         want = torch.arange(1, P + 1, device="cuda", dtype=torch.float32).repeat_interleave(recv)
         assert all(torch.equal(x, want) for x in g)
     lb.finalize()
-os.environ["DDL_TMA_MIN_SLICE_BYTES"] = "0"
-g = ddl.InProcessGroup(2, [2], max_bytes=1 << 20)
-os.environ.pop("DDL_TMA_MIN_SLICE_BYTES", None)
-for algo in (ddl.ALGO_LL, ddl.ALGO_ONESHOT, ddl.ALGO_HIER):
-    g.set_algo(algo, 1 << 19)
-    for n in (5, 4099):
-        for dt in (torch.float32, torch.bfloat16):
-            zc = [g.buffer(r, n, dt) for r in range(2)]
-            for r in range(2):
-                zc[r].fill_(r + 1)
-            st = [torch.full((n,), r + 1.0, dtype=dt, device="cuda") for r in range(2)]
-            g.all_reduce(zc)
-            g.all_reduce(st)
-            check(zc, 3)
-            check(st, 3)
-g.finalize()
+def run_group(force):
+    """the multi-process launch path (2 in-process communicators): LL, one-shot, hierarchical"""
+    os.environ.update(force)
+    g = ddl.InProcessGroup(2, [2], max_bytes=1 << 20)
+    for k in force:
+        os.environ.pop(k, None)
+    for algo in (ddl.ALGO_LL, ddl.ALGO_ONESHOT, ddl.ALGO_HIER):
+        g.set_algo(algo, 1 << 19)
+        for n in (5, 4099):
+            for dt in (torch.float32, torch.bfloat16):
+                zc = [g.buffer(r, n, dt) for r in range(2)]
+                for r in range(2):
+                    zc[r].fill_(r + 1)
+                st = [torch.full((n,), r + 1.0, dtype=dt, device="cuda") for r in range(2)]
+                g.all_reduce(zc)
+                g.all_reduce(st)
+                check(zc, 3)
+                check(st, 3)
+    g.finalize()
+
+
+run_group(TMA)
+run_group(WAVES)
 for n in (1001, (32 << 20) // 4 + 3):   # register path, then the TMA-ring path (>= 32 MiB)
     ins = [torch.full((n,), float(j), device="cuda") for j in range(3)]
     out = torch.empty(n, device="cuda")
