@@ -147,6 +147,20 @@ ddl_result_t ddl_deregister(ddl_comm_t comm, int reg_id);
 ddl_result_t ddl_allreduce(ddl_comm_t comm, void* buf, size_t count, ddl_dtype_t dtype,
                            ddl_op_t op, void* stream);
 
+/* Grouped all-reduce: nbufs independent in-place all-reduces (e.g. the gradient buckets of
+ * one SGD step) in as few launches as possible.  bufs[i] holds counts[i]
+ * elements (16-B aligned; counts[i] == 0 is skipped); every rank passes the same nbufs and
+ * counts in the same order.  Buffers in the LL / one-shot size regime, staged (not
+ * symmetric / registered) buffers, and every buffer under DDL_CHECK are all-reduced first
+ * by single ddl_allreduce calls, in order; the remaining zero-copy buffers share one launch
+ * per 8 buffers, split over DDL_CHANNELS (default 2) channels of CTAs that each run their
+ * buffers' hierarchical schedules one after another, so that one channel's barrier waits
+ * and L2-bound phases overlap another's HBM / NVLink-bound phases.  Results are
+ * bit-identical to nbufs single ddl_allreduce calls (same fold order per element).  Same
+ * errors as ddl_allreduce; asynchronous on stream. */
+ddl_result_t ddl_allreduce_many(ddl_comm_t comm, void* const* bufs, const size_t* counts, int nbufs,
+                                ddl_dtype_t dtype, ddl_op_t op, void* stream);
+
 /* NCCL layout: sendbuf holds nranks * recvcount elements; rank r receives elements
  * [r*recvcount, (r+1)*recvcount) of the reduced vector.  sendbuf is not modified.
  * The partial sums live in the workspace: nranks * recvcount * size <= max_bytes.  A
@@ -218,6 +232,11 @@ ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, in
  * each); in place. */
 ddl_result_t ddl_group_allreduce(ddl_comm_t comm, void* const* bufs, size_t count, ddl_dtype_t dtype,
                                  ddl_op_t op, void* stream);
+/* Grouped all-reduce in loopback: bufs[i * nranks + r] is virtual rank r's copy of buffer i
+ * (counts[i] elements); otherwise as ddl_allreduce_many (one-shot-sized buffers by single
+ * ddl_group_allreduce calls first, the rest in one cooperative launch per 8 buffers). */
+ddl_result_t ddl_group_allreduce_many(ddl_comm_t comm, void* const* bufs, const size_t* counts, int nbufs,
+                                      ddl_dtype_t dtype, ddl_op_t op, void* stream);
 /* sendbufs[r]: nranks*recvcount elements (not modified); recvbufs[r]: recvcount.
  * Uses a library workspace of nranks * nranks * recvcount elements (grown on demand). */
 ddl_result_t ddl_group_reduce_scatter(ddl_comm_t comm, const void* const* sendbufs, void* const* recvbufs,

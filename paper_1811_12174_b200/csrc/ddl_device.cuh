@@ -890,6 +890,93 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
   rank_epoch_end(p, me, ew, STEAL ? 2 * L : 0);
 }
 
+// ------------------------------------------------------------------------ grouped all-reduce
+// Several independent buffers ("buckets", e.g. DDP gradient buckets) all-reduced by ONE
+// launch.  The grid is split into channels (contiguous CTA ranges); channel ch runs its
+// buckets one after another, each with the full hierarchical schedule of a4-a7 on its own
+// CTAs (CTA c of a channel handles slice c of every block of the bucket), so one channel's
+// L2-bound phases and barrier waits overlap another channel's DRAM-bound phases.  Per bucket
+// the fold order is that of a single ddl_allreduce (only the slicing differs), so results
+// are bit-identical to it.  Bucket k of a channel releases epoch e+k (the rank epoch advances
+// by the longest channel's bucket count); zero-copy buffers only (no copy-in), so barrier 0
+// runs only before a channel's first bucket (and not at all in loopback).
+constexpr int kMaxBuckets = 8;
+constexpr int kMaxChannels = 4;
+struct MBucket {
+  uint64_t n, q, slice;
+  void* buf[kMaxRanks];  // every rank's copy (loopback: the virtual ranks' buffers; else peer-mapped)
+};
+struct MParams {
+  KParams p;
+  MBucket b[kMaxBuckets];
+  int nchan;
+  int cta0[kMaxChannels + 1];  // channel ch owns CTAs [cta0[ch], cta0[ch+1])
+  int bk0[kMaxChannels + 1];   // and runs buckets order[bk0[ch] .. bk0[ch+1]) in that order
+  int order[kMaxBuckets];
+  int maxk;                    // most buckets in one channel
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(const __grid_constant__ MParams mp) {
+  pdl_begin();
+  __shared__ KParams sp;  // this CTA's working copy: per bucket n, q, slice and buffers change
+  const KParams& p0 = mp.p;
+  const int me = p0.loopback ? (int)blockIdx.y : p0.rank;
+  const uint32_t e = rank_epoch_begin(p0, me);
+  if (me == p0.skip_rank) return;
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&p0);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&sp);
+    for (uint32_t i = threadIdx.x; i < sizeof(KParams) / 4; i += blockDim.x) dst[i] = src[i];
+  }
+  int ch = 0;
+  while ((int)blockIdx.x >= mp.cta0[ch + 1]) ++ch;
+  const int lc = (int)blockIdx.x - mp.cta0[ch];
+  const Topo& t = p0.t;
+  const int L = t.nlive;
+  const int me_ = me;
+  auto group_peer = [&](int j) { return [&t, me_, j](int l) { return barrier_peer(t, me_, j, l); }; };
+  Pipe pp;
+  pipe_init(pp);  // (its __syncthreads also publishes sp)
+  const int nk = mp.bk0[ch + 1] - mp.bk0[ch];
+  uint32_t ew = e;
+#pragma unroll 1
+  for (int k = 0; k < nk; ++k) {
+    ew = e + (uint32_t)k;
+    const MBucket& B = mp.b[mp.order[mp.bk0[ch] + k]];
+    __syncthreads();  // the previous bucket's readers of sp are done
+    if (threadIdx.x == 0) {
+      sp.n = B.n;
+      sp.q = B.q;
+      sp.slice = B.slice;
+    }
+    if ((int)threadIdx.x < t.P) {
+      sp.in[threadIdx.x] = B.buf[threadIdx.x];
+      sp.work[threadIdx.x] = B.buf[threadIdx.x];
+      sp.out[threadIdx.x] = B.buf[threadIdx.x];
+    }
+    __syncthreads();
+    const KParams& p = sp;
+    for (int j = 0; j < L; ++j) {
+      if (!(j == 0 && (k > 0 || p0.loopback)) && !dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j)))
+        return;
+      PhaseCtx x = phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1);
+      x.s = lc;
+      tma_phase<T>(p, me, x, pp);
+    }
+    for (int jj = 0; jj < L; ++jj) {
+      const int j = L + jj;
+      if (!dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j))) return;
+      PhaseCtx x = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false);
+      x.s = lc;
+      tma_phase<T>(p, me, x, pp);
+    }
+  }
+  if (nk > 0 && L > 0 && !p0.loopback && !dbarrier(sp, me, 2 * L, barrier_npeers(t, 2 * L), ew, group_peer(2 * L)))
+    return;
+  rank_epoch_end(p0, me, e + (uint32_t)(mp.maxk > 0 ? mp.maxk - 1 : 0), 0);
+}
+
 // ------------------------------------------------------------------------ one-shot (a9)
 // Every rank reads slice c of all P inputs, folds them in the nested order of the live dims
 // (level j folds consecutive groups of g_{live[j]} values, rounding at each level like a

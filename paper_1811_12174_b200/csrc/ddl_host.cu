@@ -146,6 +146,7 @@ struct ddl_comm {
   int gpu_share = 1;        // ranks sharing this GPU (loopback: P; in-process test groups: P)
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
+  int channels = 2;                        // DDL_CHANNELS: channels of a grouped all-reduce
   int waves = 0;                           // DDL_WAVES: slices per CTA per hierarchical call (0 = auto)
   size_t wave_slice_bytes = 112 << 10;     // auto: target per-CTA slice of one wave
   size_t min_wave_slice_bytes = 16 << 10;  // no waves below this slice size
@@ -185,6 +186,10 @@ struct ddl_comm {
   size_t ll_slot = 0;
   char* ll_of(int r) const { return scratch_of(r) + 2 * scratch_half; }
 };
+
+extern "C" {
+static void preload_kernels();
+}
 
 namespace {
 
@@ -246,6 +251,9 @@ void apply_env(ddl_comm* c) {
   c->tma_min_slice_bytes = env_size("DDL_TMA_MIN_SLICE_BYTES", c->tma_min_slice_bytes);
   c->ll_max = env_size("DDL_LL_MAX_BYTES", c->ll_max);
   c->use_pdl = env_size("DDL_PDL", 1) != 0;
+  c->channels = (int)env_size("DDL_CHANNELS", c->channels);
+  if (c->channels < 1) c->channels = 1;
+  if (c->channels > kMaxChannels) c->channels = kMaxChannels;
   c->waves = (int)env_size("DDL_WAVES", c->waves);
   if (c->waves > 64) c->waves = 64;
   c->wave_slice_bytes = env_size("DDL_WAVE_SLICE_BYTES", c->wave_slice_bytes);
@@ -280,6 +288,7 @@ ddl_result_t common_init(ddl_comm* c, int nranks, const int* dims, int ndims, in
                        (size_t)c->cmax * kMaxRanks;             // + DDL_CHECK signatures
   c->flags_bytes = (words * 4 + 65535) / 65536 * 65536;
   apply_env(c);
+  preload_kernels();
   if (env_size("DDL_TRACE", 0)) {
     const size_t tb = (size_t)nranks * c->cmax * kTraceEvents * sizeof(uint64_t);
     DDL_CUDA(cudaMalloc(&c->trace, tb));
@@ -549,7 +558,7 @@ ddl_result_t local_copy(const void* src, void* dst, size_t count, ddl_dtype_t dt
 
 extern "C" {
 
-int ddl_version(void) { return 101; }  // 1.01: LL one-shot, ddl_set_ll_max
+int ddl_version(void) { return 102; }  // 1.02: grouped all-reduce (ddl_allreduce_many)
 
 const char* ddl_result_string(ddl_result_t r) {
   switch (r) {
@@ -935,6 +944,13 @@ ddl_result_t ddl_debug_connect_local(ddl_comm_t* comms, int nranks) {
     ddl_comm* c = comms[r];
     for (int m = 0; m < nranks; ++m) c->peer_base[m] = m == r ? nullptr : comms[m]->alloc;
     c->gpu_share = nranks;
+    // The P ranks' kernels share this GPU's SMs from P streams.  Each kernel is sized to a
+    // 1/P share (cap_per_rank), so one kernel per rank always fits -- but programmatic
+    // dependent launch could let a rank's NEXT kernel take SM slots early (waiting in
+    // griddepcontrol.wait) while another rank's current kernel still needs them.  Plain
+    // stream order here (with one GPU per rank, as in production, this cannot starve: a
+    // dependent grid only launches after every CTA of its predecessor is resident).
+    c->use_pdl = false;
     c->connected = true;
   }
   return DDL_SUCCESS;
@@ -1100,6 +1116,192 @@ static ddl_result_t check_ptrs(const ddl_comm* c, const void* const* ptrs) {
   for (int r = 0; r < c->P; ++r)
     if (!ptrs[r] || !aligned16(ptrs[r])) return DDL_ERR_INVALID_ARGUMENT;
   return DDL_SUCCESS;
+}
+
+// ---------------------------------------------------------------- grouped all-reduce (one launch)
+static const void* multi_fn_dt(ddl_dtype_t dt) {
+  if (dt == DDL_INT32) return (const void*)ddl_multi_kernel<int32_t>;
+  if (dt == DDL_FLOAT32) return (const void*)ddl_multi_kernel<float>;
+  return (const void*)ddl_multi_kernel<__nv_bfloat16>;
+}
+
+// Launch the grouped kernel for buckets i < nb with element counts ns[i] and every rank's
+// buffer ptrs[i * P + m] (hierarchical-sized, 16-B aligned, zero-copy), at most kMaxBuckets
+// per launch.  Buckets go to channels longest-first onto the least-loaded channel; each
+// channel gets CTAs in proportion to its bytes and runs its buckets in their given order.
+static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* const* ptrs, int nb, ddl_dtype_t dt,
+                                 ddl_op_t op, void* stream) {
+  const void* fn = multi_fn_dt(dt);
+  blocks_per_sm(fn, kTmaSmem);
+  const int C = cap_per_rank(c, fn, kTmaSmem);
+  const int w = elem_size(dt);
+  const uint64_t W = 16 / w;
+  for (int g0 = 0; g0 < nb; g0 += kMaxBuckets) {
+    const int gn = std::min(kMaxBuckets, nb - g0);
+    MParams mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.p = base_params(c, 0, op);
+    mp.p.mode = kRS | kAG;
+    int K = std::min(std::min(c->channels, gn), std::min(C, kMaxChannels));
+    if (K < 1) K = 1;
+    int idx[kMaxBuckets], chan_of[kMaxBuckets];
+    uint64_t load[kMaxChannels] = {0};
+    for (int i = 0; i < gn; ++i) idx[i] = i;
+    std::stable_sort(idx, idx + gn, [&](int a, int b) { return ns[g0 + a] > ns[g0 + b]; });
+    for (int j = 0; j < gn; ++j) {
+      int best = 0;
+      for (int ch = 1; ch < K; ++ch)
+        if (load[ch] < load[best]) best = ch;
+      chan_of[idx[j]] = best;
+      load[best] += ns[g0 + idx[j]];
+    }
+    uint64_t total = 0;
+    for (int ch = 0; ch < K; ++ch) total += load[ch];
+    int cc[kMaxChannels], used = 0;
+    for (int ch = 0; ch < K; ++ch) {
+      cc[ch] = std::max(1, (int)((double)C * (double)load[ch] / (double)(total ? total : 1)));
+      used += cc[ch];
+    }
+    while (used > C) {  // (rounding up to 1 CTA can overshoot)
+      int big = 0;
+      for (int ch = 1; ch < K; ++ch)
+        if (cc[ch] > cc[big]) big = ch;
+      --cc[big];
+      --used;
+    }
+    while (used < C) {  // leftovers to the channel with the most bytes per CTA
+      int best = 0;
+      for (int ch = 1; ch < K; ++ch)
+        if ((double)load[ch] / cc[ch] > (double)load[best] / cc[best]) best = ch;
+      ++cc[best];
+      ++used;
+    }
+    mp.nchan = K;
+    int pos = 0, maxk = 0;
+    for (int ch = 0; ch <= kMaxChannels; ++ch) {
+      mp.cta0[ch] = ch == 0 ? 0 : mp.cta0[ch - 1] + (ch - 1 < K ? cc[ch - 1] : 0);
+      if (ch < kMaxChannels) mp.bk0[ch] = pos;
+      if (ch < K) {
+        int k = 0;
+        for (int i = 0; i < gn; ++i)
+          if (chan_of[i] == ch) {
+            mp.order[pos++] = i;
+            ++k;
+          }
+        maxk = std::max(maxk, k);
+      }
+    }
+    mp.bk0[kMaxChannels] = pos;
+    mp.maxk = maxk;
+    for (int i = 0; i < gn; ++i) {
+      const uint64_t n = ns[g0 + i];
+      const uint64_t q = block_elems(n, c->P, w);
+      uint64_t slice = (q + cc[chan_of[i]] - 1) / cc[chan_of[i]];
+      slice = (slice + W - 1) / W * W;
+      mp.b[i].n = n;
+      mp.b[i].q = q;
+      mp.b[i].slice = slice ? slice : W;
+      for (int m = 0; m < c->P; ++m) mp.b[i].buf[m] = ptrs[(size_t)(g0 + i) * c->P + m];
+    }
+    void* args[] = {&mp};
+    if (c->debug)
+      std::fprintf(stderr, "[ddl] multi: %d buckets, %d channels, ctas %d (%d/%d/%d/%d), maxk %d\n", gn, K, C,
+                   cc[0], K > 1 ? cc[1] : 0, K > 2 ? cc[2] : 0, K > 3 ? cc[3] : 0, maxk);
+    DDL_CUDA(launch_ex(fn, c->loopback ? dim3(C, c->P) : dim3(C), kTmaSmem, static_cast<cudaStream_t>(stream), args,
+                       c->loopback, c->use_pdl));
+  }
+  return DDL_SUCCESS;
+}
+
+// Load every kernel of the library once per process, at the first communicator.  With CUDA's
+// lazy module loading a kernel's first launch (or occupancy query) loads it, which can wait
+// for the device to go idle -- and a device-side barrier kernel already running waits for a
+// peer's launch that the blocked host thread has not issued yet (seen with several ranks in
+// one process: a timeout on the first call of a new kernel).  Loading up front also keeps
+// the load off the first call's latency.
+static void preload_kernels() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    std::vector<const void*> fns;
+    for (ddl_dtype_t dt : {DDL_INT32, DDL_FLOAT32, DDL_BFLOAT16}) {
+      for (int path = 0; path <= 6; ++path) fns.push_back(hier_fn_dt(dt, path));
+      for (int K = 1; K <= 4; ++K) {
+        fns.push_back(ll_fn_dt(dt, K));
+        for (int R : {1, 2, 4}) fns.push_back(oneshot_fn_dt(dt, K, R));
+      }
+      fns.push_back(multi_fn_dt(dt));
+    }
+    fns.push_back((const void*)ddl_local_reduce_kernel<int32_t, true>);
+    fns.push_back((const void*)ddl_local_reduce_kernel<int32_t, false>);
+    fns.push_back((const void*)ddl_local_reduce_kernel<float, true>);
+    fns.push_back((const void*)ddl_local_reduce_kernel<float, false>);
+    fns.push_back((const void*)ddl_local_reduce_kernel<__nv_bfloat16, true>);
+    fns.push_back((const void*)ddl_local_reduce_kernel<__nv_bfloat16, false>);
+    fns.push_back((const void*)ddl_local_reduce_tma_kernel<int32_t>);
+    fns.push_back((const void*)ddl_local_reduce_tma_kernel<float>);
+    fns.push_back((const void*)ddl_local_reduce_tma_kernel<__nv_bfloat16>);
+    for (const void* fn : fns) {
+      cudaFuncAttributes a;
+      if (fn) (void)cudaFuncGetAttributes(&a, fn);
+    }
+    (void)cudaGetLastError();
+  });
+}
+
+ddl_result_t ddl_group_allreduce_many(ddl_comm_t c, void* const* bufs, const size_t* counts, int nbufs,
+                                      ddl_dtype_t dt, ddl_op_t op, void* stream) {
+  ddl_result_t r = check_common(c, dt, op);
+  if (r != DDL_SUCCESS) return r;
+  if (!c->loopback || nbufs < 0 || (nbufs > 0 && (!bufs || !counts))) return DDL_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < nbufs; ++i)
+    if (counts[i] && (r = check_ptrs(c, bufs + (size_t)i * c->P)) != DDL_SUCCESS) return r;
+  if (c->P == 1) return DDL_SUCCESS;
+  DDL_ON_DEVICE(c->device);
+  // small buckets (one-shot regime) and empty ones go through single calls first, in order
+  std::vector<uint64_t> ns;
+  std::vector<void*> ptrs;
+  for (int i = 0; i < nbufs; ++i) {
+    if (!counts[i]) continue;
+    Plan pl;
+    if (use_oneshot(c, counts[i], dt, &pl)) {
+      if ((r = ddl_group_allreduce(c, bufs + (size_t)i * c->P, counts[i], dt, op, stream)) != DDL_SUCCESS) return r;
+      continue;
+    }
+    ns.push_back(counts[i]);
+    for (int m = 0; m < c->P; ++m) ptrs.push_back(bufs[(size_t)i * c->P + m]);
+  }
+  if (ns.empty()) return DDL_SUCCESS;
+  return launch_multi(c, ns.data(), ptrs.data(), (int)ns.size(), dt, op, stream);
+}
+
+ddl_result_t ddl_allreduce_many(ddl_comm_t c, void* const* bufs, const size_t* counts, int nbufs, ddl_dtype_t dt,
+                                ddl_op_t op, void* stream) {
+  ddl_result_t r = check_common(c, dt, op);
+  if (r != DDL_SUCCESS) return r;
+  if (c->loopback || nbufs < 0 || (nbufs > 0 && (!bufs || !counts))) return DDL_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < nbufs; ++i)
+    if (counts[i] && (!bufs[i] || !aligned16(bufs[i]))) return DDL_ERR_INVALID_ARGUMENT;
+  if (c->P == 1) return DDL_SUCCESS;
+  DDL_ON_DEVICE(c->device);
+  // buckets that are not zero-copy (staged), in the LL / one-shot regime, or checked with
+  // DDL_CHECK go through single calls first, in order; the rest share one launch
+  std::vector<uint64_t> ns;
+  std::vector<void*> ptrs;
+  for (int i = 0; i < nbufs; ++i) {
+    if (!counts[i]) continue;
+    const char* peer[kMaxRanks];
+    Plan pl;
+    const bool single = c->check || use_ll(c, counts[i], dt, &pl) || use_oneshot(c, counts[i], dt, &pl) ||
+                        !zero_copy_peers(c, bufs[i], counts[i] * elem_size(dt), peer);
+    if (single) {
+      if ((r = ddl_allreduce(c, bufs[i], counts[i], dt, op, stream)) != DDL_SUCCESS) return r;
+      continue;
+    }
+    ns.push_back(counts[i]);
+    for (int m = 0; m < c->P; ++m) ptrs.push_back(const_cast<char*>(peer[m]));
+  }
+  if (ns.empty()) return DDL_SUCCESS;
+  return launch_multi(c, ns.data(), ptrs.data(), (int)ns.size(), dt, op, stream);
 }
 
 ddl_result_t ddl_group_allreduce(ddl_comm_t c, void* const* bufs, size_t count, ddl_dtype_t dt, ddl_op_t op,

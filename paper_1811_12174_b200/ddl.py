@@ -67,6 +67,7 @@ def _load() -> ctypes.CDLL:
         "ddl_connect": (c_int, [c_void, c_void]),
         "ddl_buffer": (c_int, [c_void, pp, ctypes.POINTER(c_size)]),
         "ddl_allreduce": (c_int, [c_void, c_void, c_size, c_int, c_int, c_void]),
+        "ddl_allreduce_many": (c_int, [c_void, pp, ctypes.POINTER(c_size), c_int, c_int, c_int, c_void]),
         "ddl_reduce_scatter": (c_int, [c_void, c_void, c_void, c_size, c_int, c_int, c_void]),
         "ddl_allgather": (c_int, [c_void, c_void, c_void, c_size, c_int, c_void]),
         "ddl_async_error": (c_int, [c_void]),
@@ -86,6 +87,7 @@ def _load() -> ctypes.CDLL:
         "ddl_finalize": (c_int, [c_void]),
         "ddl_loopback_init": (c_int, [pp, c_int, ip, c_int, c_int]),
         "ddl_group_allreduce": (c_int, [c_void, pp, c_size, c_int, c_int, c_void]),
+        "ddl_group_allreduce_many": (c_int, [c_void, pp, ctypes.POINTER(c_size), c_int, c_int, c_int, c_void]),
         "ddl_group_reduce_scatter": (c_int, [c_void, pp, pp, c_size, c_int, c_int, c_void]),
         "ddl_group_allgather": (c_int, [c_void, pp, pp, c_size, c_int, c_void]),
         "ddl_local_reduce": (c_int, [pp, c_int, c_void, c_size, c_int, ctypes.c_float, c_void]),
@@ -115,6 +117,10 @@ def _ints(xs) -> ctypes.Array:
 
 def _ptrs(xs) -> ctypes.Array:
     return (ctypes.c_void_p * max(1, len(xs)))(*xs)
+
+
+def _sizes(xs) -> ctypes.Array:
+    return (ctypes.c_size_t * max(1, len(xs)))(*xs)
 
 
 def parse_dims(spec, nranks: int | None = None) -> list[int]:
@@ -285,6 +291,32 @@ class Comm:
                                       _stream(stream, t.device.index)), "ddl_allreduce")
         return t
 
+    def all_reduce_many(self, ts, op: str = "sum", stream=None):
+        """Grouped in-place all-reduce of several tensors of one dtype (e.g. the gradient
+        buckets of a step): zero-copy ones share one launch over DDL_CHANNELS channels
+        (``ddl_allreduce_many``); results equal one all_reduce per tensor bit for bit.
+        Every rank passes the same tensor sizes in the same order."""
+        if not ts:
+            return ts
+        dt = dtype_name(ts[0])
+        rest = []
+        for t in ts:
+            _require_cuda(t)
+            if dtype_name(t) != dt:
+                raise DDLError(ERR_INVALID_ARGUMENT, "all_reduce_many: mixed dtypes")
+            nbytes = t.numel() * t.element_size()
+            inside = self.buffer_ptr <= t.data_ptr() and t.data_ptr() + nbytes <= self.buffer_ptr + self.buffer_bytes
+            if not inside and nbytes > self.buffer_bytes:
+                self.all_reduce(t, op, stream)   # staged in workspace-sized pieces
+            else:
+                rest.append(t)
+        if rest:
+            _check(_lib.ddl_allreduce_many(self.h, _ptrs([t.data_ptr() for t in rest]),
+                                           _sizes([t.numel() for t in rest]), len(rest), DTYPE_CODES[dt],
+                                           OP_CODES[op], _stream(stream, rest[0].device.index)),
+                   "ddl_allreduce_many")
+        return ts
+
     def register(self, t) -> int:
         """Collective: register a persistent device tensor (same size on every rank) so that
         all-reduces on it -- or on a view at the same offset on every rank -- are zero-copy."""
@@ -414,6 +446,25 @@ class Loopback:
                "ddl_group_allreduce")
         return bufs
 
+    def all_reduce_many(self, buckets, op: str = "sum", stream=None):
+        """Grouped all-reduce: buckets[i][r] is virtual rank r's copy of buffer i (one dtype);
+        one cooperative launch for the hierarchical-sized buffers (``ddl_group_allreduce_many``)."""
+        if not buckets:
+            return buckets
+        dt = dtype_name(buckets[0][0])
+        ptrs = []
+        for b in buckets:
+            if len(b) != self.nranks or any(dtype_name(t) != dt or t.numel() != b[0].numel() for t in b):
+                raise DDLError(ERR_INVALID_ARGUMENT, "all_reduce_many: one same-size tensor per rank per bucket")
+            for t in b:
+                _require_cuda(t)
+            ptrs += [t.data_ptr() for t in b]
+        _check(_lib.ddl_group_allreduce_many(self.h, _ptrs(ptrs), _sizes([b[0].numel() for b in buckets]),
+                                             len(buckets), DTYPE_CODES[dt], OP_CODES[op],
+                                             _stream(stream, buckets[0][0].device.index)),
+               "ddl_group_allreduce_many")
+        return buckets
+
     def reduce_scatter(self, outs, inps, op: str = "sum", stream=None):
         _check(_lib.ddl_group_reduce_scatter(self.h, _ptrs([t.data_ptr() for t in inps]),
                                              _ptrs([t.data_ptr() for t in outs]), outs[0].numel(),
@@ -523,6 +574,15 @@ class InProcessGroup:
         self._each(lambda r, s: _check(_lib.ddl_allreduce(self.hs[r], bufs[r].data_ptr(), bufs[r].numel(), dt,
                                                           OP_CODES[op], s), "ddl_allreduce"))
         return bufs
+
+    def all_reduce_many(self, buckets, op: str = "sum"):
+        """buckets[i][r]: rank r's tensor of bucket i; every rank calls ddl_allreduce_many."""
+        dt = DTYPE_CODES[dtype_name(buckets[0][0])]
+        sizes = _sizes([b[0].numel() for b in buckets])
+        self._each(lambda r, s: _check(_lib.ddl_allreduce_many(self.hs[r], _ptrs([b[r].data_ptr() for b in buckets]),
+                                                               sizes, len(buckets), dt, OP_CODES[op], s),
+                                       "ddl_allreduce_many"))
+        return buckets
 
     def reduce_scatter(self, outs, inps, op: str = "sum"):
         dt = DTYPE_CODES[dtype_name(outs[0])]

@@ -1,0 +1,155 @@
+"""GPU parity of the grouped all-reduce (ddl_allreduce_many / ddl_group_allreduce_many): several
+buckets in one launch, split over channels of CTAs.  Every bucket must equal the oracle's
+all-reduce of that bucket bit for bit (same fold order as a single call), across
+factorisations, dtypes, ragged and one-shot-sized buckets mixed in, more buckets than one
+launch holds, every channel count, interleaved with single calls (epoch bookkeeping), on the
+loopback and the multi-process launch paths, and under CUDA-graph replay."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic_inputs as si
+from gpu_util import to_dev, to_host, same_bits, first_diff
+from paper_1811_12174_b200 import ddl
+
+pytestmark = pytest.mark.gpu
+
+KIND = {"int32": "fullrange", "float32": "normal", "bfloat16": "normal"}
+# hierarchical-sized buckets (grouped) mixed with one-shot-sized and empty ones (single calls)
+SIZES = [300_001, 1_000_003, 7, 2_000_000, 0, 600_000, 123_457]
+
+
+def with_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def check_buckets(devs, hosts, dims, dtype, op, tag):
+    P = len(hosts[0])
+    for i, (dv, hv) in enumerate(zip(devs, hosts)):
+        if hv[0].size == 0:
+            continue
+        want = oracle.allreduce(hv, dims, dtype, op)
+        for r in range(P):
+            got = to_host(dv[r])
+            assert same_bits(got, want[r]), (tag, i, hv[0].size, r, first_diff(got, want[r]))
+
+
+def make(P, dtype, sizes, seed):
+    hosts = [si.rank_buffers(dtype, KIND[dtype], n, P, seed=seed + i) for i, n in enumerate(sizes)]
+    devs = [[to_dev(h, dtype) for h in hv] for hv in hosts]
+    return hosts, devs
+
+
+@pytest.mark.parametrize("P,dims", [(8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (4, [2, 2]), (6, [3, 2])])
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_loopback_grouped_matches_oracle(P, dims, dtype):
+    lb = ddl.Loopback(P, dims)
+    op = "sum" if dtype == "int32" else "avg"
+    hosts, devs = make(P, dtype, SIZES, seed=100)
+    lb.all_reduce_many(devs, op)
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    check_buckets(devs, hosts, dims, dtype, op, "loopback")
+    lb.finalize()
+
+
+@pytest.mark.parametrize("channels", ["1", "3", "4"])
+def test_loopback_grouped_channels_and_split(channels):
+    """11 hierarchical-sized buckets (two launches of <= 8) on 1, 3 and 4 channels."""
+    P, dims = 8, [4, 2]
+    lb = with_env({"DDL_CHANNELS": channels}, lambda: ddl.Loopback(P, dims))
+    sizes = [200_003 + 37_011 * i for i in range(11)]
+    hosts, devs = make(P, "float32", sizes, seed=7)
+    lb.all_reduce_many(devs, "sum")
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    check_buckets(devs, hosts, dims, "float32", "sum", f"channels={channels}")
+    lb.finalize()
+
+
+def test_loopback_grouped_interleaved_with_single_calls():
+    """Grouped calls advance the rank epoch by their longest channel's bucket count; single
+    calls (hierarchical with waves, one-shot) before and after must still synchronise."""
+    P, dims = 8, [4, 2]
+    lb = ddl.Loopback(P, dims)
+    rng = np.random.Generator(np.random.PCG64(5))
+    for it in range(6):
+        sizes = [int(x) for x in rng.choice([150_001, 700_000, 1_500_017, 40_000], size=int(rng.integers(2, 6)))]
+        hosts, devs = make(P, "int32", sizes, seed=1000 + 10 * it)
+        lb.all_reduce_many(devs, "sum")
+        n1 = int(rng.choice([1000, 300_000, 9_000_001]))
+        single = si.rank_buffers("int32", "fullrange", n1, P, seed=it)
+        sd = [to_dev(b, "int32") for b in single]
+        lb.all_reduce(sd, "sum")
+        torch.cuda.synchronize()
+        assert lb.async_error() == ddl.SUCCESS
+        check_buckets(devs, hosts, dims, "int32", "sum", f"it={it}")
+        want = oracle.naive_sum(single, "int32")
+        assert all(np.array_equal(to_host(t), want) for t in sd), it
+    lb.finalize()
+
+
+def test_loopback_grouped_graph_replay():
+    P, dims = 8, [2, 2, 2]
+    lb = ddl.Loopback(P, dims)
+    sizes = [400_000, 1_200_000, 900_001]
+    bufs = [[torch.zeros(n, device="cuda") for _ in range(P)] for n in sizes]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            lb.all_reduce_many(bufs, "avg")
+    torch.cuda.synchronize()
+    for it in range(3):
+        hosts = [si.rank_buffers("float32", "normal", n, P, seed=60 + 5 * it + i) for i, n in enumerate(sizes)]
+        for b, hv in zip(bufs, hosts):
+            for r in range(P):
+                b[r].copy_(to_dev(hv[r], "float32"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert lb.async_error() == ddl.SUCCESS
+        check_buckets(bufs, hosts, dims, "float32", "avg", f"replay {it}")
+    lb.finalize()
+
+
+@pytest.mark.parametrize("P,dims", [(2, [2]), (4, [2, 2]), (8, [4, 2])])
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_multiprocess_path_grouped(P, dims, dtype):
+    """The multi-process launch path (P communicators in this process): buckets in the
+    symmetric buffer share one launch per rank; a staged bucket and an LL-sized bucket in the
+    same call go through single calls."""
+    g = with_env({"DDL_TIMEOUT_MS": "5000"}, lambda: ddl.InProcessGroup(P, dims, max_bytes=32 << 20))
+    op = "sum" if dtype == "int32" else "avg"
+    sizes = [700_001, 1_000, 1_300_000, 300_000, 2_000_003]
+    hosts = [si.rank_buffers(dtype, KIND[dtype], n, P, seed=300 + i) for i, n in enumerate(sizes)]
+    esz = 4 if dtype != "bfloat16" else 2
+    tdt = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}[dtype]
+    bufs, off = [], 0
+    for i, hv in enumerate(hosts):
+        n = hv[0].size
+        if i == 3:   # staged (outside the symmetric buffer)
+            bufs.append([to_dev(h, dtype) for h in hv])
+            continue
+        views = [g.buffer(r, n, tdt, off) for r in range(P)]
+        for r in range(P):
+            views[r].copy_(to_dev(hv[r], dtype))
+        bufs.append(views)
+        off += (n * esz + 255) // 256 * 256
+    g.all_reduce_many(bufs, op)
+    torch.cuda.synchronize()
+    assert g.async_error() == ddl.SUCCESS
+    check_buckets(bufs, hosts, dims, dtype, op, "inproc")
+    g.finalize()
