@@ -44,6 +44,9 @@ NVLINK_MEASURED_PEER = 770.0   # B200_PROFILING.md: measured peer copy per direc
 DIMS_FOR_N = {1: "2x4", 2: "2", 4: "2x2", 8: "2x4"}
 
 
+TRAFFIC_KEY = "resnet50-grad-set 8 virtual ranks dims 2x4 avg, grouped"
+
+
 def profiled_traffic(workload_key: str):
     """DRAM bytes per step of the timed kernels from the committed ncu capture
     (profiles/traffic.json, written from an `ncu --set full` run of scripts/profile_step.py)."""
@@ -219,7 +222,13 @@ def run_loopback(args):
     S_total = sum(sizes) * 4
     stream = torch.cuda.current_stream()
 
-    def step(evs=None):
+    # One step = the whole gradient set: the 5 buckets in ONE grouped all-reduce
+    # (ddl_group_allreduce_many: each bucket runs the full 2x4 schedule; the buckets share
+    # the launch over DDL_CHANNELS channels of CTAs).  Bit-identical to 5 single calls.
+    def step():
+        lb.all_reduce_many(bufs, "avg")
+
+    def seq_step(evs=None):   # the same set as 5 single calls (context: "sequential")
         for b in range(nb):
             if evs is not None:
                 evs[b][0].record(stream)
@@ -227,7 +236,6 @@ def run_loopback(args):
             if evs is not None:
                 evs[b][1].record(stream)
 
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nb)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:   # sampling spans warm-up + timed region (>= a few 100-ms samples)
         for _ in range(args.warmup):
@@ -240,18 +248,46 @@ def run_loopback(args):
         while time.perf_counter() - t_pad < 0.3:   # keep the GPU busy so the sampler sees load clocks
             step()
             torch.cuda.synchronize()
+        # the timed region: exactly K steps between two events, nothing else on the stream
         t_start.record(stream)
         for k in range(args.steps):
-            step(evs[k])
+            step()
         t_end.record(stream)
+        torch.cuda.synchronize()
+        # kernel durations for the roofline: a second pass of K steps with an event pair
+        # around every launch (an event between launches costs ~2-3 us of GPU time, so it
+        # stays out of the headline region)
+        kev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        for k in range(args.steps):
+            kev[k][0].record(stream)
+            step()
+            kev[k][1].record(stream)
+        torch.cuda.synchronize()
+        # context: the same set as 5 single calls, per-bucket events
+        sev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nb)] for _ in range(args.steps)]
+        for k in range(args.steps):
+            seq_step(sev[k])
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for k in range(args.steps):
+            seq_step()
+        s1.record(stream)
         torch.cuda.synchronize()
     assert lb.async_error() == ddl.SUCCESS
     ms = t_start.elapsed_time(t_end) / args.steps
     busbw = S_total * 2 * (P - 1) / P / (ms * 1e-3) / 1e9
-    kern_ms = sum(evs[k][b][0].elapsed_time(evs[k][b][1]) for k in range(args.steps) for b in range(nb))
-    bucket_us = [sum(evs[k][b][0].elapsed_time(evs[k][b][1]) for k in range(args.steps)) / args.steps * 1e3
+    kern_ms = sum(kev[k][0].elapsed_time(kev[k][1]) for k in range(args.steps))
+    seq_ms = s0.elapsed_time(s1) / args.steps
+    bucket_us = [sum(sev[k][b][0].elapsed_time(sev[k][b][1]) for k in range(args.steps)) / args.steps * 1e3
                  for b in range(nb)]
-    algo_bytes = sum(loopback_hbm_bytes(n, P, dims, 4) for n in sizes) * args.steps
+    n_oneshot = sum(1 for s in sizes if lb.algo_for(s, "float32") == ddl.ALGO_ONESHOT)
+    launches_per_step = n_oneshot + -(-(nb - n_oneshot) // 8)
+    # Roofline numerator: the all-reduce's COMPULSORY HBM bytes in one GPU -- every virtual
+    # rank's input read once and its result written once, 2 * P * S per step (as K5's
+    # (g+1)*n*w).  The schedule's own phase bytes (27/8 * S per rank for 2x4, many of them
+    # L2 hits) are reported beside it; against the copy peak they exceed 1.
+    algo_bytes = 2 * P * S_total * args.steps
+    sched_bytes = sum(loopback_hbm_bytes(n, P, dims, 4) for n in sizes) * args.steps
     hbm_peak, peak_src = peaks()
     achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
 
@@ -315,26 +351,33 @@ def run_loopback(args):
                    "dims": "x".join(map(str, dims[::-1])), "n_ranks": P, "bytes_per_rank": S_total,
                    "buckets": sizes, "l2": "inputs (8 x 102 MB) larger than L2, no flush",
                    "algo": ["oneshot" if lb.algo_for(s, "float32") == ddl.ALGO_ONESHOT else "hier" for s in sizes],
-                   "ctas_per_rank": [lb.ctas_for(s, "float32") for s in sizes],
-                   "bucket_us": [round(u, 1) for u in bucket_us]},
+                   "step": "one grouped all-reduce of the 5 buckets (ddl_group_allreduce_many, "
+                           f"{os.environ.get('DDL_CHANNELS', '2')} channels, {launches_per_step} launch(es))",
+                   "sequential": {"ms_per_step": round(seq_ms, 4), "calls": "5 single ddl_group_allreduce",
+                                  "ctas_per_rank": [lb.ctas_for(s, "float32") for s in sizes],
+                                  "bucket_us": [round(u, 1) for u in bucket_us]}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
-                     "traffic": (tr // nb if (tr := profiled_traffic("resnet50-grad-set 8 virtual ranks dims 2x4 avg"))
+                     "traffic": (tr // launches_per_step if (tr := profiled_traffic(TRAFFIC_KEY))
                                  and dims == [4, 2] else None),
-                     "traffic_unit": "DRAM bytes per launch (mean of the 5 bucket launches of one step), "
-                                     "ncu --set full, profiles/traffic.json",
-                     "algorithmic_bytes_per_launch": algo_bytes // args.steps // nb,
+                     "traffic_unit": "DRAM bytes per launch, ncu --set full of one bench step, profiles/traffic.json",
+                     "algorithmic_bytes_per_launch": algo_bytes // args.steps // launches_per_step,
                      "peak_source": peak_src,
-                     "kernel": "ddl_hier_kernel<float,2> (TMA-staged; loopback, all 8 virtual ranks in one launch)",
+                     "kernel": "ddl_multi_kernel<float> (grouped: 5 buckets x 8 virtual ranks in one launch, "
+                               "TMA-staged phases)",
+                     "kernel_timing": "second pass of K steps, CUDA events around every launch",
+                     "algorithmic_bytes": "compulsory: 2 x 8 virtual ranks x 102,228,128 B per step "
+                                          "(each input read once, each result written once)",
                      "algorithmic_bytes_per_step": algo_bytes // args.steps,
+                     "schedule_bytes_per_step": sched_bytes // args.steps,
+                     "schedule_frac": sched_bytes / (kern_ms * 1e-3) / 1e9 / hbm_peak,
                      "kernel_ms_per_step": kern_ms / args.steps,
                      # physical view: profiled DRAM bytes of a step / this run's kernel time
                      "dram_frac": ((tr2 / (kern_ms / args.steps * 1e-3) / 1e9 / hbm_peak)
-                                   if (tr2 := profiled_traffic("resnet50-grad-set 8 virtual ranks dims 2x4 avg"))
-                                   and dims == [4, 2] else None)},
+                                   if (tr2 := profiled_traffic(TRAFFIC_KEY)) and dims == [4, 2] else None)},
         "e2e": {"value": S_total * 2 * (P - 1) / P / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": S_total * P, "d2h_bytes_per_step": S_total},
-        "gpu_launches": nb * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "local_reduce": {"g": g, "bytes": (g + 1) * n5 * 4, "ms": k5_ms, "achieved": k5_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": k5_gbs / hbm_peak},

@@ -24,10 +24,10 @@ launches = [{"kernel": r[col["Kernel Name"]], "grid": r[col["Grid Size"]],
              "dram_pct": float(r[col["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]]),
              "l2_hit_pct": float(r[col["lts__t_sector_hit_rate.pct"]])} for r in data]
 out = {"source": f"ncu --set full --clock-control none, {details} ({len(launches)} launches = one bench step)",
-       "kernel": "ddl_hier_kernel<float,2> (TMA-staged)",
+       "kernel": launches[0]["kernel"] if launches else None,
        "dram_bytes_per_step": sum(l["dram_bytes"] for l in launches),
        "ncu_kernel_us_per_step": round(sum(l["us"] for l in launches), 3),
-       "workload": "resnet50-grad-set 8 virtual ranks dims 2x4 avg",
+       "workload": "resnet50-grad-set 8 virtual ranks dims 2x4 avg, grouped",
        "launches": launches}
 with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json"), "w") as f:
     json.dump(out, f, indent=1)
