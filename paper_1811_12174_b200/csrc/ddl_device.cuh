@@ -903,7 +903,8 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
 constexpr int kMaxBuckets = 8;
 constexpr int kMaxChannels = 4;
 struct MBucket {
-  uint64_t n, q, slice;
+  uint64_t n, q, slice;  // slice: per CTA per wave
+  int nwaves;            // waves of this bucket (slice w * channel CTAs + c in wave w)
   void* buf[kMaxRanks];  // every rank's copy (loopback: the virtual ranks' buffers; else peer-mapped)
 };
 struct MParams {
@@ -913,7 +914,7 @@ struct MParams {
   int cta0[kMaxChannels + 1];  // channel ch owns CTAs [cta0[ch], cta0[ch+1])
   int bk0[kMaxChannels + 1];   // and runs buckets order[bk0[ch] .. bk0[ch+1]) in that order
   int order[kMaxBuckets];
-  int maxk;                    // most buckets in one channel
+  int maxk;                    // most bucket-waves in one channel
 };
 
 template <typename T>
@@ -938,12 +939,17 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
   auto group_peer = [&](int j) { return [&t, me_, j](int l) { return barrier_peer(t, me_, j, l); }; };
   Pipe pp;
   pipe_init(pp);  // (its __syncthreads also publishes sp)
+  const int cc = mp.cta0[ch + 1] - mp.cta0[ch];
   const int nk = mp.bk0[ch + 1] - mp.bk0[ch];
   uint32_t ew = e;
+  int seq = 0;  // bucket-waves done by this channel
 #pragma unroll 1
-  for (int k = 0; k < nk; ++k) {
+  for (int kw = 0; kw < nk; ++kw) {
+    const MBucket& B = mp.b[mp.order[mp.bk0[ch] + kw]];
+#pragma unroll 1
+    for (int w = 0; w < (B.nwaves > 1 ? B.nwaves : 1); ++w, ++seq) {
+    const int k = seq;
     ew = e + (uint32_t)k;
-    const MBucket& B = mp.b[mp.order[mp.bk0[ch] + k]];
     __syncthreads();  // the previous bucket's readers of sp are done
     if (threadIdx.x == 0) {
       sp.n = B.n;
@@ -961,15 +967,16 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
       if (!(j == 0 && (k > 0 || p0.loopback)) && !dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j)))
         return;
       PhaseCtx x = phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1);
-      x.s = lc;
+      x.s = w * cc + lc;
       tma_phase<T>(p, me, x, pp);
     }
     for (int jj = 0; jj < L; ++jj) {
       const int j = L + jj;
       if (!dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j))) return;
       PhaseCtx x = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false);
-      x.s = lc;
+      x.s = w * cc + lc;
       tma_phase<T>(p, me, x, pp);
+    }
     }
   }
   if (nk > 0 && L > 0 && !p0.loopback && !dbarrier(sp, me, 2 * L, barrier_npeers(t, 2 * L), ew, group_peer(2 * L)))

@@ -147,6 +147,7 @@ struct ddl_comm {
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
   int channels = 2;                        // DDL_CHANNELS: channels of a grouped all-reduce
+  int group_waves = 1;                     // DDL_GROUP_WAVES: waves per bucket in a grouped all-reduce (0 = auto)
   int waves = 0;                           // DDL_WAVES: slices per CTA per hierarchical call (0 = auto)
   size_t wave_slice_bytes = 112 << 10;     // auto: target per-CTA slice of one wave
   size_t min_wave_slice_bytes = 16 << 10;  // no waves below this slice size
@@ -252,6 +253,7 @@ void apply_env(ddl_comm* c) {
   c->ll_max = env_size("DDL_LL_MAX_BYTES", c->ll_max);
   c->use_pdl = env_size("DDL_PDL", 1) != 0;
   c->channels = (int)env_size("DDL_CHANNELS", c->channels);
+  c->group_waves = (int)env_size("DDL_GROUP_WAVES", c->group_waves);
   if (c->channels < 1) c->channels = 1;
   if (c->channels > kMaxChannels) c->channels = kMaxChannels;
   c->waves = (int)env_size("DDL_WAVES", c->waves);
@@ -1193,16 +1195,41 @@ static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* co
     }
     mp.bk0[kMaxChannels] = pos;
     mp.maxk = maxk;
+    int waves_of[kMaxBuckets];
     for (int i = 0; i < gn; ++i) {
       const uint64_t n = ns[g0 + i];
       const uint64_t q = block_elems(n, c->P, w);
-      uint64_t slice = (q + cc[chan_of[i]] - 1) / cc[chan_of[i]];
+      const int nc = cc[chan_of[i]];
+      uint64_t slice = (q + nc - 1) / nc;
       slice = (slice + W - 1) / W * W;
+      int nw = 1;
+      // Waves per bucket (DDL_GROUP_WAVES; 0 = auto: about one per wave_slice_bytes of per-CTA
+      // slice, rounded): a smaller working set per wave keeps more partials in L2 while the
+      // other channels stream.
+      int gw = c->group_waves;
+      if (gw == 0) gw = (int)std::min<uint64_t>(32, (slice * w + c->wave_slice_bytes / 2) / c->wave_slice_bytes);
+      if (gw > 1) {
+        uint64_t s2 = (q + (uint64_t)nc * gw - 1) / ((uint64_t)nc * gw);
+        s2 = (s2 + W - 1) / W * W;
+        if (s2 * w >= c->min_wave_slice_bytes) {
+          slice = s2;
+          nw = (int)((q + (uint64_t)nc * s2 - 1) / ((uint64_t)nc * s2));
+        }
+      }
+      waves_of[i] = nw;
       mp.b[i].n = n;
       mp.b[i].q = q;
+      mp.b[i].nwaves = nw;
       mp.b[i].slice = slice ? slice : W;
       for (int m = 0; m < c->P; ++m) mp.b[i].buf[m] = ptrs[(size_t)(g0 + i) * c->P + m];
     }
+    mp.maxk = 0;
+    for (int ch = 0; ch < K; ++ch) {
+      int kw = 0;
+      for (int j = mp.bk0[ch]; j < mp.bk0[ch + 1]; ++j) kw += waves_of[mp.order[j]];
+      mp.maxk = std::max(mp.maxk, kw);
+    }
+    maxk = mp.maxk;
     void* args[] = {&mp};
     if (c->debug)
       std::fprintf(stderr, "[ddl] multi: %d buckets, %d channels, ctas %d (%d/%d/%d/%d), maxk %d\n", gn, K, C,

@@ -65,11 +65,13 @@ def test_loopback_grouped_matches_oracle(P, dims, dtype):
     lb.finalize()
 
 
-@pytest.mark.parametrize("channels", ["1", "3", "4"])
-def test_loopback_grouped_channels_and_split(channels):
-    """11 hierarchical-sized buckets (two launches of <= 8) on 1, 3 and 4 channels."""
+@pytest.mark.parametrize("channels,waves", [("1", "1"), ("3", "1"), ("4", "1"), ("2", "3"), ("3", "0")])
+def test_loopback_grouped_channels_and_split(channels, waves):
+    """11 hierarchical-sized buckets (two launches of <= 8) on 1-4 channels, with and without
+    waves per bucket (DDL_GROUP_WAVES, 0 = auto)."""
     P, dims = 8, [4, 2]
-    lb = with_env({"DDL_CHANNELS": channels}, lambda: ddl.Loopback(P, dims))
+    lb = with_env({"DDL_CHANNELS": channels, "DDL_GROUP_WAVES": waves, "DDL_MIN_WAVE_SLICE_BYTES": "0"},
+                  lambda: ddl.Loopback(P, dims))
     sizes = [200_003 + 37_011 * i for i in range(11)]
     hosts, devs = make(P, "float32", sizes, seed=7)
     lb.all_reduce_many(devs, "sum")
