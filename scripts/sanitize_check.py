@@ -39,6 +39,19 @@ for (P, dims), force in runs:
         want = torch.arange(1, P + 1, device="cuda", dtype=torch.float32).repeat_interleave(recv)
         assert all(torch.equal(x, want) for x in g)
     lb.finalize()
+# grouped all-reduce (one launch, channels; waves per bucket too)
+for force in ({}, {"DDL_GROUP_WAVES": "2", "DDL_MIN_WAVE_SLICE_BYTES": "0", "DDL_CHANNELS": "3"}):
+    os.environ.update(force)
+    lb = ddl.Loopback(8, [4, 2])
+    for k in force:
+        os.environ.pop(k, None)
+    bk = [[torch.full((n,), r + 1.0, device="cuda") for r in range(8)] for n in (70_001, 160_003, 99_999, 5)]
+    lb.all_reduce_many(bk)
+    for b in bk:
+        check(b, 36)
+    lb.finalize()
+
+
 def run_group(force):
     """the multi-process launch path (2 in-process communicators): LL, one-shot, hierarchical"""
     os.environ.update(force)
