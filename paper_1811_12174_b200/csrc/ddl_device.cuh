@@ -66,6 +66,12 @@ struct KParams {
   const void* cin[kMaxRanks];   // copy-in source of each rank
   void* cout[kMaxRanks];        // copy-out destination of each rank
   int mode;
+  int l2hint;          // L2 eviction priorities (default 15): bit 0: the first RS phase's inputs
+                       // loaded evict_first (each is read once); bit 1: allgather stores
+                       // evict_first (final, never re-read in the call); bit 2: later RS phases'
+                       // loads evict_first (partials, consumed); bit 3: non-last RS phases' stores
+                       // evict_last (partials the next phase reads); bit 4: also the last RS
+                       // phase's stores (off: they would linger as evict_last after the call)
   int nwaves;          // hier: slices per CTA, run one after another (wave w = slice w*gridDim.x + blockIdx.x)
   uint64_t* trace;     // debug (DDL_TRACE=1): [P][cmax][kTraceEvents] globaltimer stamps, else null
   int stream_every;    // PATH 5: publish progress every k chunks (and at the phase end)
@@ -181,6 +187,11 @@ __device__ __forceinline__ void st_elem(char* p, uint32_t v) {
 }
 __device__ __forceinline__ uint4 ld_vec(const char* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ void st_vec(char* p, const uint4& v) { *reinterpret_cast<uint4*>(p) = v; }
+__device__ __forceinline__ void st_vec_hint(char* p, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(pol)
+               : "memory");
+}
 
 // ------------------------------------------------------------------------ device barrier (K4)
 // Flag signal / poll.  Across GPUs the scope must be .sys; in loopback mode every agent is
@@ -630,6 +641,30 @@ __device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t 
                ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// The same with an L2 eviction-priority policy (createpolicy).
+__device__ __forceinline__ void tma_load_hint(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_store_hint(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 // Bulk store shared -> global (async proxy), grouped per thread.
 __device__ __forceinline__ void tma_store(void* gdst, const void* ssrc, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
@@ -699,7 +734,10 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
     char* sbase = pp.smem + (size_t)st * kStageBytes;
     const size_t go = ud.e0 * sizeof(T) + poff;
     mbar_arm(&pp.bar[st], bytes * (uint32_t)x.g);
-    if (x.kind == kPhRS) {
+    if (x.kind == kPhRS && ((x.first && (p.l2hint & 1)) || (!x.first && (p.l2hint & 4)))) {
+      const uint64_t pol = policy_evict_first();
+      for (int v = 0; v < x.g; ++v) tma_load_hint(sbase + (size_t)v * CB, s_srcs[v] + go, bytes, &pp.bar[st], pol);
+    } else if (x.kind == kPhRS) {
       for (int v = 0; v < x.g; ++v) tma_load(sbase + (size_t)v * CB, s_srcs[v] + go, bytes, &pp.bar[st]);
     } else {
       tma_load(sbase, ud.src + go, bytes, &pp.bar[st]);
@@ -726,6 +764,11 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
     mbar_wait(&pp.bar[st], (sq / kStages) & 1u);
     const uint32_t nv = bytes / 16u;
     if (x.kind == kPhRS) {
+      // partials of a non-last RS phase are read again by the next phase (and later
+      // overwritten): keep them in L2 (evict_last, bit 3); the last phase's results keep the
+      // normal priority unless bit 4 (they would otherwise linger as evict_last after the call)
+      const bool keep = (p.l2hint & 8) && (!x.last || (p.l2hint & 16));
+      const uint64_t pol_last = keep ? policy_evict_last() : 0;
       for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
         A acc[W];
         unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)i * 16), acc);
@@ -739,12 +782,14 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
 #pragma unroll
           for (int k = 0; k < W; ++k) acc[k] = Tr<T>::mul(acc[k], p.scale);
         }
-        st_vec(pd + (size_t)i * 16, pack<T>(acc));
+        if (keep) st_vec_hint(pd + (size_t)i * 16, pack<T>(acc), pol_last);
+        else st_vec(pd + (size_t)i * 16, pack<T>(acc));
       }
     } else if (threadIdx.x == 0) {
       // copy: one bulk store from the stage (async proxy); the stage is reusable once the
       // store has read it
-      tma_store(pd, sbase, bytes);
+      if (x.kind == kPhAG && (p.l2hint & 2)) tma_store_hint(pd, sbase, bytes, policy_evict_first());
+      else tma_store(pd, sbase, bytes);
       tma_store_wait_read();
     }
     coff += bytes;

@@ -147,6 +147,7 @@ struct ddl_comm {
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
   int channels = 2;                        // DDL_CHANNELS: channels of a grouped all-reduce
+  int l2hint = 15;                         // DDL_L2_HINTS: KParams::l2hint bits (profiles/r01_l2_hints.txt)
   int group_waves = 1;                     // DDL_GROUP_WAVES: waves per bucket in a grouped all-reduce (0 = auto)
   int waves = 0;                           // DDL_WAVES: slices per CTA per hierarchical call (0 = auto)
   size_t wave_slice_bytes = 112 << 10;     // auto: target per-CTA slice of one wave
@@ -254,6 +255,7 @@ void apply_env(ddl_comm* c) {
   c->use_pdl = env_size("DDL_PDL", 1) != 0;
   c->channels = (int)env_size("DDL_CHANNELS", c->channels);
   c->group_waves = (int)env_size("DDL_GROUP_WAVES", c->group_waves);
+  c->l2hint = (int)env_size("DDL_L2_HINTS", c->l2hint);
   if (c->channels < 1) c->channels = 1;
   if (c->channels > kMaxChannels) c->channels = kMaxChannels;
   c->waves = (int)env_size("DDL_WAVES", c->waves);
@@ -487,6 +489,7 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
   p.err = c->err;
   p.trace = c->trace;
   p.stream_every = c->stream_every;
+  p.l2hint = c->l2hint;
   for (int r = 0; r < c->P; ++r) p.flags[r] = c->flags_of(r);
   return p;
 }
