@@ -8,8 +8,10 @@
 Every row is preceded by a correctness gate: all ranks bit-identical, and for
 integer-valued inputs equal to the closed form P*(P+1)/2 (no oracle on this path).
 Timing: CUDA-graph replay of `iters` calls (device time, no host launch cost), CUDA events,
-max over ranks.  Columns: impl,P,dims,dtype,op,bytes,us,algbw_GBs,busbw_GBs,pct_roof,roof
-(roof = HBM copy peak for loopback rows -- against the schedule's algorithmic HBM bytes --
+max over ranks.  Columns: impl,P,dims,dtype,op,bytes,us,algbw_GBs,busbw_GBs,pct_roof,roof[,sched_pct]
+(roof = HBM copy peak for loopback rows -- against the all-reduce's compulsory HBM bytes 2*P*S
+(every virtual rank's input read once, its result written once); sched_pct uses the
+schedule's phase bytes instead, many of them L2 hits, so it can pass 100 --
 and 900 GB/s NVLink for N > 1).  The P = 1 rows of config 5 are the K5 local reduce (g = 8
 buffers of S bytes -> 1): algbw column = (g+1)*S / t against the HBM peak.
 """
@@ -105,7 +107,8 @@ def loopback(args, out):
         hb = bench.loopback_hbm_bytes(n, P, dims, w)
         algo = "oneshot" if lb.algo_for(n, dtype) == ddl.ALGO_ONESHOT else "hier"
         row = ["ddl-loopback-" + algo, P, spec, dtype, op, S, f"{us:.2f}", f"{S / us / 1e3:.2f}",
-               f"{S * 2 * (P - 1) / P / us / 1e3:.2f}", f"{hb / us / 1e3 / hbm * 100:.1f}", "hbm"]
+               f"{S * 2 * (P - 1) / P / us / 1e3:.2f}", f"{2 * P * S / us / 1e3 / hbm * 100:.1f}", "hbm",
+               f"{hb / us / 1e3 / hbm * 100:.1f}"]
         print(",".join(map(str, row)), file=out, flush=True)
         del bufs
 
@@ -180,7 +183,7 @@ def main():
     args = ap.parse_args()
     out = open(args.out, "a") if args.out else sys.stdout
     if int(os.environ.get("RANK", "0")) == 0 and (not args.out or os.path.getsize(args.out) == 0):
-        print("impl,P,dims,dtype,op,bytes,us,algbw_GBs,busbw_GBs,pct_roof,roof", file=out, flush=True)
+        print("impl,P,dims,dtype,op,bytes,us,algbw_GBs,busbw_GBs,pct_roof,roof,sched_pct", file=out, flush=True)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         multi(args, out)
     else:
