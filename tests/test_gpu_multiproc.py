@@ -76,6 +76,19 @@ def _rank_main(rank, world, port, q, env, dims):
         comm.all_reduce(view, "avg")
         torch.cuda.synchronize()
         res["registered"] = (same_bits(to_host(view), oracle.allreduce(rb, dims, "float32", "avg")[rank]),)
+        # grouped all-reduce (one launch for the zero-copy buckets, .sys flags across processes):
+        # two buckets in the symmetric buffer, one in the registered buffer, one LL-sized, one staged
+        gsz = [400_003, 700_000, 120_000, 999, 80_001]
+        gb = [si.rank_buffers("float32", "normal", n, world, seed=40 + i) for i, n in enumerate(gsz)]
+        views = [comm.buffer(gsz[0], torch.float32, 0), comm.buffer(gsz[1], torch.float32, 1_600_256),
+                 reg[4096:4096 + gsz[2]], comm.buffer(gsz[3], torch.float32, 4_800_000),
+                 torch.zeros(gsz[4], device="cuda")]
+        for v, b in zip(views, gb):
+            v.copy_(to_dev(b[rank], "float32"))
+        comm.all_reduce_many(views, "avg")
+        torch.cuda.synchronize()
+        res["grouped"] = tuple(same_bits(to_host(v), oracle.allreduce(b, dims, "float32", "avg")[rank])
+                               for v, b in zip(views, gb))
         res["err"] = comm.async_error()
         comm.finalize()
     except Exception as e:  # report, don't hang the parent
@@ -109,5 +122,5 @@ def test_processes_ipc_one_gpu(world, dims, env):
     for r in range(world):
         assert "exc" not in out[r], out[r]
         assert out[r]["err"] == 0
-        for dtype in ("float32", "int32", "bfloat16", "ll", "big", "registered"):
+        for dtype in ("float32", "int32", "bfloat16", "ll", "big", "registered", "grouped"):
             assert all(out[r][dtype]), (r, dtype)
