@@ -155,3 +155,18 @@ def test_multiprocess_path_grouped(P, dims, dtype):
     assert g.async_error() == ddl.SUCCESS
     check_buckets(bufs, hosts, dims, dtype, op, "inproc")
     g.finalize()
+
+
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_loopback_grouped_tiny_buckets_forced_hierarchical(dtype):
+    """DDL_ALGO=hier sends even 1-element buckets through the grouped kernel: most CTAs get
+    empty slices, the rest ragged element-wise tails."""
+    P, dims = 8, [2, 2, 2]
+    lb = with_env({"DDL_ALGO": "hier"}, lambda: ddl.Loopback(P, dims))
+    op = "sum" if dtype == "int32" else "avg"
+    hosts, devs = make(P, dtype, [1, 7, 33, 1000, 4097], seed=77)
+    lb.all_reduce_many(devs, op)
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    check_buckets(devs, hosts, dims, dtype, op, "tiny")
+    lb.finalize()
