@@ -984,6 +984,12 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
   auto group_peer = [&](int j) { return [&t, me_, j](int l) { return barrier_peer(t, me_, j, l); }; };
   Pipe pp;
   pipe_init(pp);  // (its __syncthreads also publishes sp)
+  trace_ev(p0, me, 0);
+  // trace (DDL_TRACE=1): event 1 + 2*(seq*2L + j) after barrier j of bucket-wave seq, +1 after its phase
+  auto tev = [&](int seq_, int j, int after) {
+    const int ev = 1 + 2 * (seq_ * 2 * t.nlive + j) + after;
+    if (ev < kTraceEvents - 1) trace_ev(p0, me, ev);
+  };
   const int cc = mp.cta0[ch + 1] - mp.cta0[ch];
   const int nk = mp.bk0[ch + 1] - mp.bk0[ch];
   uint32_t ew = e;
@@ -1011,16 +1017,20 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
     for (int j = 0; j < L; ++j) {
       if (!(j == 0 && (k > 0 || p0.loopback)) && !dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j)))
         return;
+      tev(k, j, 0);
       PhaseCtx x = phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1);
       x.s = w * cc + lc;
       tma_phase<T>(p, me, x, pp);
+      tev(k, j, 1);
     }
     for (int jj = 0; jj < L; ++jj) {
       const int j = L + jj;
       if (!dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j))) return;
+      tev(k, j, 0);
       PhaseCtx x = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false);
       x.s = w * cc + lc;
       tma_phase<T>(p, me, x, pp);
+      tev(k, j, 1);
     }
     }
   }
