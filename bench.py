@@ -376,7 +376,9 @@ def run_loopback(args):
                      "dram_frac": ((tr2 / (kern_ms / args.steps * 1e-3) / 1e9 / hbm_peak)
                                    if (tr2 := profiled_traffic(TRAFFIC_KEY)) and dims == [4, 2] else None)},
         "e2e": {"value": S_total * 2 * (P - 1) / P / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
-                "ms_per_step": e2e_ms, "h2d_bytes_per_step": S_total * P, "d2h_bytes_per_step": S_total},
+                "ms_per_step": e2e_ms, "h2d_bytes_per_step": S_total * P, "d2h_bytes_per_step": S_total,
+                "how": "per bucket, pipelined on three streams: pinned H2D of the 8 ranks' copies || "
+                       "ddl_group_allreduce || D2H of the reduced bucket (PCIe-bound)"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "local_reduce": {"g": g, "bytes": (g + 1) * n5 * 4, "ms": k5_ms, "achieved": k5_gbs, "peak": hbm_peak,
