@@ -149,8 +149,8 @@ ddl_result_t ddl_allreduce(ddl_comm_t comm, void* buf, size_t count, ddl_dtype_t
 
 /* Grouped all-reduce: nbufs independent in-place all-reduces (e.g. the gradient buckets of
  * one SGD step) in as few launches as possible.  bufs[i] holds counts[i]
- * elements (16-B aligned; counts[i] == 0 is skipped); every rank passes the same nbufs and
- * counts in the same order.  Buffers in the LL / one-shot size regime, staged (not
+ * elements (16-B aligned, not overlapping one another; counts[i] == 0 is skipped); every
+ * rank passes the same nbufs and counts in the same order.  Buffers in the LL / one-shot size regime, staged (not
  * symmetric / registered) buffers, and every buffer under DDL_CHECK are all-reduced first
  * by single ddl_allreduce calls, in order; the remaining zero-copy buffers share one launch
  * per 8 buffers, split over DDL_CHANNELS (default 2) channels of CTAs that each run their
