@@ -66,6 +66,8 @@ struct KParams {
   const void* cin[kMaxRanks];   // copy-in source of each rank
   void* cout[kMaxRanks];        // copy-out destination of each rank
   int mode;
+  int transposed;      // loopback hierarchical / grouped kernels: grid (P, ctas) -- blockIdx.x is the
+                       // rank, .y the CTA, so a slice chain's P CTAs are dispatched back to back
   int l2hint;          // L2 eviction priorities (default 15): bit 0: the first RS phase's inputs
                        // loaded evict_first (each is read once); bit 1: allgather stores
                        // evict_first (final, never re-read in the call); bit 2: later RS phases'
@@ -83,16 +85,21 @@ struct KParams {
 };
 constexpr int kTraceEvents = 40;
 
+// This CTA's index within its rank and the rank's CTA count (the grid is (ctas, P) in
+// loopback, or transposed to (P, ctas) for the grouped kernel with DDL_TRANSPOSE=1).
+__device__ __forceinline__ int cta_id(const KParams& p) { return p.transposed ? (int)blockIdx.y : (int)blockIdx.x; }
+__device__ __forceinline__ int cta_count(const KParams& p) { return p.transposed ? (int)gridDim.y : (int)gridDim.x; }
+
 // Debug timeline: thread 0 of each CTA stamps the global timer at event ev.
 __device__ __forceinline__ void trace_ev(const KParams& p, int me, int ev) {
   if (p.trace && threadIdx.x == 0) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[((size_t)me * p.cmax + blockIdx.x) * kTraceEvents + ev] = t;
+    p.trace[((size_t)me * p.cmax + cta_id(p)) * kTraceEvents + ev] = t;
     if (ev == 0) {
       uint32_t smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      p.trace[((size_t)me * p.cmax + blockIdx.x) * kTraceEvents + kTraceEvents - 1] = smid;
+      p.trace[((size_t)me * p.cmax + cta_id(p)) * kTraceEvents + kTraceEvents - 1] = smid;
     }
   }
 }
@@ -230,9 +237,9 @@ __device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int
   if (threadIdx.x < np) {
     const int m = peer(threadIdx.x);
     const bool chk = check_sig && p.sig;
-    if (chk) *(volatile uint32_t*)sig_slot(p, p.flags[m], blockIdx.x, me) = p.sig;
-    st_release(flag_slot(p, p.flags[m], slot, blockIdx.x, me), epoch, p.gpu_scope);
-    const uint32_t* f = flag_slot(p, p.flags[me], slot, blockIdx.x, m);
+    if (chk) *(volatile uint32_t*)sig_slot(p, p.flags[m], cta_id(p), me) = p.sig;
+    st_release(flag_slot(p, p.flags[m], slot, cta_id(p), me), epoch, p.gpu_scope);
+    const uint32_t* f = flag_slot(p, p.flags[me], slot, cta_id(p), m);
     uint64_t t0 = 0;
     uint32_t spins = 0;
     while ((int32_t)(ld_acquire(f, p.gpu_scope) - epoch) < 0) {
@@ -246,7 +253,7 @@ __device__ __forceinline__ bool dbarrier(const KParams& p, int me, int slot, int
         }
       }
     }
-    if (!fail && chk && *(volatile uint32_t*)sig_slot(p, p.flags[me], blockIdx.x, m) != p.sig) {
+    if (!fail && chk && *(volatile uint32_t*)sig_slot(p, p.flags[me], cta_id(p), m) != p.sig) {
       atomicCAS(p.err, 0, kErrMismatch);  // ranks disagree on (count, dtype, op, algorithm)
       fail = 1;
     }
@@ -311,13 +318,13 @@ __device__ __forceinline__ void rank_epoch_end(const KParams& p, int me, uint32_
   if (threadIdx.x == 0) {
     uint32_t* sb = steal_base(p, me);
     const uint32_t old = atom_add_acq_rel_gpu(sb, 1);
-    s_last = (old == gridDim.x - 1);
+    s_last = (old == (uint32_t)cta_count(p) - 1);
     if (s_last) *sb = 0;
   }
   __syncthreads();
   if (s_last) {
     for (int j = 0; j < steal_phases; ++j)
-      for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+      for (uint32_t i = threadIdx.x; i < (uint32_t)cta_count(p); i += blockDim.x) {
         steal_tick(p, me, j)[i] = 0;
         steal_done(p, me, j)[i] = 0;
       }
@@ -375,7 +382,7 @@ __device__ __forceinline__ PhaseCtx phase_ctx(const KParams& p, int me, int kind
   x.c = 0;
   x.nb = 0;
   x.g = 1;
-  x.s = blockIdx.x;
+  x.s = cta_id(p);
   if (kind == kPhRS) {
     x.g = t.g[d];
     x.nb = nblocks(t, d + 1);
@@ -820,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
   constexpr bool STEAL = PATH == 4;
   constexpr bool STREAM = PATH == 5;
   constexpr bool WAVES = PATH == 6;
-  const int me = p.loopback ? (int)blockIdx.y : p.rank;
+  const int me = p.loopback ? (p.transposed ? (int)blockIdx.x : (int)blockIdx.y) : p.rank;
   const uint32_t e = rank_epoch_begin(p, me);
   if (me == p.skip_rank) return;
   const Topo& t = p.t;
@@ -881,7 +888,7 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
 #pragma unroll 1
   for (int w = 0; w < nw; ++w) {
     ew = e + (uint32_t)w;
-    const int sidx = w * (int)gridDim.x + (int)blockIdx.x;
+    const int sidx = w * cta_count(p) + cta_id(p);
     const bool tr = w == nw - 1;
     auto ctx = [&](int kind, int d, bool first, bool last) {
       PhaseCtx x = phase_ctx(p, me, kind, d, first, last);
@@ -967,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
   pdl_begin();
   __shared__ KParams sp;  // this CTA's working copy: per bucket n, q, slice and buffers change
   const KParams& p0 = mp.p;
-  const int me = p0.loopback ? (int)blockIdx.y : p0.rank;
+  const int me = p0.loopback ? (p0.transposed ? (int)blockIdx.x : (int)blockIdx.y) : p0.rank;
   const uint32_t e = rank_epoch_begin(p0, me);
   if (me == p0.skip_rank) return;
   {
@@ -976,8 +983,9 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
     for (uint32_t i = threadIdx.x; i < sizeof(KParams) / 4; i += blockDim.x) dst[i] = src[i];
   }
   int ch = 0;
-  while ((int)blockIdx.x >= mp.cta0[ch + 1]) ++ch;
-  const int lc = (int)blockIdx.x - mp.cta0[ch];
+  const int cid = cta_id(p0);
+  while (cid >= mp.cta0[ch + 1]) ++ch;
+  const int lc = cid - mp.cta0[ch];
   const Topo& t = p0.t;
   const int L = t.nlive;
   const int me_ = me;

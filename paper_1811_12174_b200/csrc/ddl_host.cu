@@ -147,6 +147,7 @@ struct ddl_comm {
   uint64_t* trace = nullptr;  // DDL_TRACE=1: per-CTA phase timeline (debug)
   size_t tma_min_slice_bytes = 16 << 10;  // TMA path only when per-CTA slices are at least this big
   int channels = 2;                        // DDL_CHANNELS: channels of a grouped all-reduce
+  int transpose = 1;                       // DDL_TRANSPOSE: loopback grids (P, ctas) (profiles/r01_transpose_ab.txt)
   int l2hint = 15;                         // DDL_L2_HINTS: KParams::l2hint bits (profiles/r01_l2_hints.txt)
   int group_waves = 1;                     // DDL_GROUP_WAVES: waves per bucket in a grouped all-reduce (0 = auto)
   int waves = 0;                           // DDL_WAVES: slices per CTA per hierarchical call (0 = auto)
@@ -256,6 +257,7 @@ void apply_env(ddl_comm* c) {
   c->channels = (int)env_size("DDL_CHANNELS", c->channels);
   c->group_waves = (int)env_size("DDL_GROUP_WAVES", c->group_waves);
   c->l2hint = (int)env_size("DDL_L2_HINTS", c->l2hint);
+  c->transpose = (int)env_size("DDL_TRANSPOSE", c->transpose);
   if (c->channels < 1) c->channels = 1;
   if (c->channels > kMaxChannels) c->channels = kMaxChannels;
   c->waves = (int)env_size("DDL_WAVES", c->waves);
@@ -518,7 +520,10 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
                  pl.ll ? "ll" : pl.oneshot ? "oneshot" : "hier", (unsigned long long)p.n, (unsigned long long)p.q,
                  (unsigned long long)p.slice, pl.nctas, p.nwaves, pl.path, p.mode, c->P, (int)c->loopback);
   if (c->loopback) {
-    DDL_CUDA(launch_ex(fn, dim3(pl.nctas, c->P), smem, s, args, true, c->use_pdl));
+    // hierarchical kernels without the experimental variants: transposed grid (DDL_TRANSPOSE)
+    const bool tr = c->transpose && !pl.oneshot && !pl.ll && (pl.path <= 2 || pl.path == 6);
+    p.transposed = tr ? 1 : 0;
+    DDL_CUDA(launch_ex(fn, tr ? dim3(c->P, pl.nctas) : dim3(pl.nctas, c->P), smem, s, args, true, c->use_pdl));
   } else {
     DDL_CUDA(launch_ex(fn, dim3(pl.nctas), smem, s, args, false, c->use_pdl));
   }
@@ -1237,8 +1242,9 @@ static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* co
     if (c->debug)
       std::fprintf(stderr, "[ddl] multi: %d buckets, %d channels, ctas %d (%d/%d/%d/%d), maxk %d\n", gn, K, C,
                    cc[0], K > 1 ? cc[1] : 0, K > 2 ? cc[2] : 0, K > 3 ? cc[3] : 0, maxk);
-    DDL_CUDA(launch_ex(fn, c->loopback ? dim3(C, c->P) : dim3(C), kTmaSmem, static_cast<cudaStream_t>(stream), args,
-                       c->loopback, c->use_pdl));
+    mp.p.transposed = (c->loopback && c->transpose) ? 1 : 0;
+    const dim3 grid = !c->loopback ? dim3(C) : mp.p.transposed ? dim3(c->P, C) : dim3(C, c->P);
+    DDL_CUDA(launch_ex(fn, grid, kTmaSmem, static_cast<cudaStream_t>(stream), args, c->loopback, c->use_pdl));
   }
   return DDL_SUCCESS;
 }
