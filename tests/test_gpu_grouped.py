@@ -65,13 +65,14 @@ def test_loopback_grouped_matches_oracle(P, dims, dtype):
     lb.finalize()
 
 
-@pytest.mark.parametrize("channels,waves", [("1", "1"), ("3", "1"), ("4", "1"), ("2", "3"), ("3", "0")])
-def test_loopback_grouped_channels_and_split(channels, waves):
+@pytest.mark.parametrize("channels,waves,transpose", [("1", "1", "1"), ("3", "1", "1"), ("4", "1", "1"),
+                                                       ("2", "3", "1"), ("3", "0", "1"), ("2", "1", "0")])
+def test_loopback_grouped_channels_and_split(channels, waves, transpose):
     """11 hierarchical-sized buckets (two launches of <= 8) on 1-4 channels, with and without
-    waves per bucket (DDL_GROUP_WAVES, 0 = auto)."""
+    waves per bucket (DDL_GROUP_WAVES, 0 = auto), transposed grid or not."""
     P, dims = 8, [4, 2]
-    lb = with_env({"DDL_CHANNELS": channels, "DDL_GROUP_WAVES": waves, "DDL_MIN_WAVE_SLICE_BYTES": "0"},
-                  lambda: ddl.Loopback(P, dims))
+    lb = with_env({"DDL_CHANNELS": channels, "DDL_GROUP_WAVES": waves, "DDL_MIN_WAVE_SLICE_BYTES": "0",
+                   "DDL_TRANSPOSE": transpose}, lambda: ddl.Loopback(P, dims))
     sizes = [200_003 + 37_011 * i for i in range(11)]
     hosts, devs = make(P, "float32", sizes, seed=7)
     lb.all_reduce_many(devs, "sum")
