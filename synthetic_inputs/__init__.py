@@ -16,6 +16,11 @@ block layout): it only draws per-rank gradient-like buffers, deterministic in
 * fp32   ``rankplus1`` : x_r[i] = r + 1.
 * bf16   ``normal``    : N(0, 1) drawn in fp32 and TRUNCATED to its upper 16 bits (returned as
   uint16 bit patterns).  Truncation, not the method's RNE cast, so no rounding code lives here.
+* fp32 / bf16 ``specials`` : IEEE special values mixed with N(0,1): about half of the
+  elements are drawn from a fixed palette of bit patterns (+-0, the smallest and largest
+  subnormals, +-max finite, +-values whose pairwise sums overflow, +-inf, quiet NaNs with
+  different payloads and signs), the rest are ``normal``.  Bit patterns are chosen, never
+  computed, so no arithmetic of the method lives here either.
 * ``resnet50`` buckets : ResNet-50's 161 parameter tensors in torch DDP's bucket order
   (resnet50_buckets.json, written by scripts/gen_resnet50_buckets.py); each tensor's values
   are N(0, (1e-2 / sqrt(fan_in))^2), the scale of a gradient at He-initialised weights.
@@ -72,6 +77,47 @@ def bf16_normal_bits(n: int, rank: int, seed: int = BASE_SEED) -> np.ndarray:
     return (f.view(np.uint32) >> 16).astype(np.uint16)
 
 
+# IEEE special bit patterns (SURVEY.md 8(c) ledger 9/10: no FTZ, NaNs compare equal)
+FP32_SPECIALS = np.array([
+    0x00000000, 0x80000000,             # +0, -0
+    0x00000001, 0x80000001,             # +- smallest subnormal
+    0x007FFFFF, 0x807FFFFF,             # +- largest subnormal
+    0x00800000,                         # smallest normal
+    0x7F7FFFFF, 0xFF7FFFFF,             # +- max finite
+    0x7F160000, 0xFF160000,             # +- 2.0e38: two of them overflow
+    0x7F800000, 0xFF800000,             # +- inf
+    0x7FC00000, 0xFFC00001, 0x7F800001,  # NaNs: canonical, negative with payload, signalling
+    0x3F800000, 0xBF800000,             # +- 1
+], dtype=np.uint32)
+
+BF16_SPECIALS = np.array([
+    0x0000, 0x8000,                     # +0, -0
+    0x0001, 0x8001,                     # +- smallest subnormal
+    0x007F, 0x807F,                     # +- largest subnormal
+    0x7F7F, 0xFF7F,                     # +- max finite
+    0x7F16, 0xFF16,                     # +- 2.0e38
+    0x7F80, 0xFF80,                     # +- inf
+    0x7FC0, 0xFFC1, 0x7F81,             # NaNs
+    0x3F80, 0xBF80,                     # +- 1
+], dtype=np.uint16)
+
+
+def fp32_specials(n: int, rank: int, seed: int = BASE_SEED) -> np.ndarray:
+    g = rng(rank, seed, 5)
+    base = g.standard_normal(n, dtype=np.float32).view(np.uint32)
+    pick = g.integers(0, len(FP32_SPECIALS), size=n)
+    use = g.random(n) < 0.5
+    return np.where(use, FP32_SPECIALS[pick], base).astype(np.uint32).view(np.float32)
+
+
+def bf16_specials_bits(n: int, rank: int, seed: int = BASE_SEED) -> np.ndarray:
+    g = rng(rank, seed, 6)
+    base = (g.standard_normal(n, dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    pick = g.integers(0, len(BF16_SPECIALS), size=n)
+    use = g.random(n) < 0.5
+    return np.where(use, BF16_SPECIALS[pick], base).astype(np.uint16)
+
+
 KINDS = {
     ("int32", "uniform"): int32_uniform,
     ("int32", "bitmask"): int32_bitmask,
@@ -80,6 +126,8 @@ KINDS = {
     ("float32", "intvalued"): fp32_intvalued,
     ("float32", "rankplus1"): fp32_rankplus1,
     ("bfloat16", "normal"): bf16_normal_bits,
+    ("float32", "specials"): fp32_specials,
+    ("bfloat16", "specials"): bf16_specials_bits,
 }
 
 

@@ -19,22 +19,37 @@ def to_host(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy()
 
 
+def _nan_mask(a: np.ndarray):
+    """NaN positions: fp32 by value, bf16 (uint16 bit patterns) when (bits & 0x7FFF) > 0x7F80."""
+    if a.dtype == np.float32:
+        return np.isnan(a)
+    if a.dtype == np.uint16:
+        return (a & 0x7FFF) > 0x7F80
+    return None
+
+
 def same_bits(a: np.ndarray, b: np.ndarray) -> bool:
-    """Bitwise equality; all NaNs compare equal (SURVEY ledger 10)."""
+    """Bitwise equality; all NaNs compare equal, fp32 and bf16 alike (SURVEY ledger 10)."""
     a = np.asarray(a)
     b = np.asarray(b)
-    if a.shape != b.shape:
+    if a.shape != b.shape or a.dtype != b.dtype:
         return False
-    if a.dtype == np.float32:
-        na, nb = np.isnan(a), np.isnan(b)
-        return bool(np.array_equal(na, nb) and np.array_equal(a.view(np.uint32)[~na], b.view(np.uint32)[~nb]))
-    return bool(np.array_equal(a, b))
+    na, nb = _nan_mask(a), _nan_mask(b)
+    if na is None:
+        return bool(np.array_equal(a, b))
+    ua = a.view(np.uint32) if a.dtype == np.float32 else a
+    ub = b.view(np.uint32) if b.dtype == np.float32 else b
+    return bool(np.array_equal(na, nb) and np.array_equal(ua[~na], ub[~nb]))
 
 
 def first_diff(a, b):
     a = np.asarray(a)
     b = np.asarray(b)
+    na, nb = _nan_mask(a), _nan_mask(b)
     if a.dtype == np.float32:
         a, b = a.view(np.uint32), b.view(np.uint32)
-    idx = np.nonzero(a != b)[0]
+    diff = a != b
+    if na is not None:
+        diff &= ~(na & nb)
+    idx = np.nonzero(diff)[0]
     return (int(idx[0]), a[idx[0]], b[idx[0]], len(idx)) if len(idx) else None

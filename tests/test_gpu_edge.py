@@ -1,0 +1,379 @@
+"""GPU parity on the method's own edge cases (VERDICT r01 "next round" 1a-d):
+
+* dims containing g_d = 1 ([4,1,2], [1,8], [8,1], [2,1,2,1,2], ...) and P = 1 -- a size-1
+  dim is a legal dim whose phase is skipped (SPEC S:L266 group_size >= 1, "1x1 ->
+  empty phase list", "1 rank -> identity"; SURVEY 8(c) ledger 13) -- through
+  every entry point: loopback hierarchical / one-shot, the multi-process launch path (LL,
+  pull one-shot, hierarchical; zero-copy and staged), reduce-scatter / allgather, and the
+  grouped all-reduce;
+* IEEE special values in fp32 and bf16 (+-0, subnormals, +-max, overflow to +-inf,
+  inf - inf, NaN; ledger 9/10: no FTZ/DAZ, all NaNs equal, everything else bitwise);
+* the bench's exact call (ddl_group_allreduce_many over the 5 full-size ResNet-50 buckets,
+  8 virtual ranks, 2x4, avg, default channels) checked against the oracle on sampled
+  elements, and the same grouped call on the multi-process launch path;
+* north_star's bf16 gate at exactly 1e-2 over EVERY element of config 4, the measured
+  maximum printed.
+
+Every comparison is against oracle/ (CPU, numpy), element by element on the same seeded
+inputs (synthetic_inputs)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic_inputs as si
+from gpu_util import to_dev, to_host, same_bits, first_diff, TORCH
+from paper_1811_12174_b200 import ddl
+
+pytestmark = pytest.mark.gpu
+
+KIND = {"int32": "fullrange", "float32": "normal", "bfloat16": "normal"}
+UNIT_DIMS = [(8, [4, 1, 2]), (8, [1, 8]), (8, [8, 1]), (8, [2, 1, 2, 1, 2]), (8, [1, 2, 4, 1]),
+             (4, [1, 2, 1, 2]), (2, [1, 2]), (2, [2, 1]), (6, [3, 1, 2])]
+UNIT_IDS = [f"P{P}-{'.'.join(map(str, d))}" for P, d in UNIT_DIMS]
+SIZES = (1, 7, 1000, 40_003, 300_001)
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _short_timeout():
+    old = os.environ.get("DDL_TIMEOUT_MS")
+    os.environ["DDL_TIMEOUT_MS"] = "5000"
+    yield
+    if old is None:
+        os.environ.pop("DDL_TIMEOUT_MS", None)
+    else:
+        os.environ["DDL_TIMEOUT_MS"] = old
+
+
+def _run_lb(lb, bufs, dtype, op):
+    dev = [to_dev(b, dtype) for b in bufs]
+    lb.all_reduce(dev, op)
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    return [to_host(t) for t in dev]
+
+
+def _cases():
+    for dtype in ("int32", "float32", "bfloat16"):
+        for op in (["sum"] if dtype == "int32" else ["sum", "avg"]):
+            yield dtype, op
+
+
+# ------------------------------------------------------------------ g_d = 1 and P = 1
+
+@pytest.mark.parametrize("P,dims", UNIT_DIMS, ids=UNIT_IDS)
+@pytest.mark.parametrize("algo", [ddl.ALGO_HIER, ddl.ALGO_ONESHOT, ddl.ALGO_AUTO], ids=["hier", "oneshot", "auto"])
+def test_unit_dims_loopback(P, dims, algo):
+    lb = ddl.Loopback(P, dims)
+    lb.set_algo(algo, 1 << 40 if algo == ddl.ALGO_ONESHOT else (512 << 10 if algo == ddl.ALGO_AUTO else 0))
+    for dtype, op in _cases():
+        for n in SIZES:
+            bufs = si.rank_buffers(dtype, KIND[dtype], n, P, seed=n + 3)
+            want = oracle.allreduce(bufs, dims, dtype, op)
+            got = _run_lb(lb, bufs, dtype, op)
+            for r in range(P):
+                assert same_bits(got[r], want[r]), (dims, algo, dtype, op, n, r, first_diff(got[r], want[r]))
+    lb.finalize()
+
+
+@pytest.mark.parametrize("P,dims", [(8, [4, 1, 2]), (8, [1, 8]), (4, [2, 1, 2]), (2, [1, 2, 1])])
+def test_unit_dims_loopback_rs_ag_grouped(P, dims):
+    lb = ddl.Loopback(P, dims)
+    recv = 65_536 + 8
+    for dtype, op in _cases():
+        bufs = si.rank_buffers(dtype, KIND[dtype], P * recv, P, seed=5)
+        want = oracle.reduce_scatter(bufs, dims, dtype, op)
+        sends = [to_dev(b, dtype) for b in bufs]
+        outs = [torch.empty(recv, dtype=TORCH[dtype], device="cuda") for _ in range(P)]
+        lb.reduce_scatter(outs, sends, op)
+        torch.cuda.synchronize()
+        for r in range(P):
+            assert same_bits(to_host(outs[r]), want[r]), ("rs", dims, dtype, op, r)
+        blocks = si.rank_buffers(dtype, KIND[dtype], recv, P, seed=6)
+        wantg = oracle.allgather(blocks, dims, dtype)
+        ins = [to_dev(b, dtype) for b in blocks]
+        outs = [torch.empty(P * recv, dtype=TORCH[dtype], device="cuda") for _ in range(P)]
+        lb.all_gather(outs, ins)
+        torch.cuda.synchronize()
+        for r in range(P):
+            assert same_bits(to_host(outs[r]), wantg[r]), ("ag", dims, dtype, r)
+        # grouped: hierarchical, one-shot-sized and empty buckets in one call
+        sizes = [300_001, 1_000_003, 7, 0, 600_000]
+        hosts = [si.rank_buffers(dtype, KIND[dtype], n, P, seed=40 + i) for i, n in enumerate(sizes)]
+        devs = [[to_dev(h, dtype) for h in hv] for hv in hosts]
+        lb.set_algo(ddl.ALGO_AUTO, 512 << 10)
+        lb.all_reduce_many(devs, op)
+        torch.cuda.synchronize()
+        assert lb.async_error() == ddl.SUCCESS
+        for i, (hv, dv) in enumerate(zip(hosts, devs)):
+            if sizes[i] == 0:
+                continue
+            w = oracle.allreduce(hv, dims, dtype, op)
+            for r in range(P):
+                assert same_bits(to_host(dv[r]), w[r]), ("grouped", dims, dtype, op, i, r)
+    lb.finalize()
+
+
+@pytest.mark.parametrize("dims", [[1], [1, 1], [1, 1, 1]])
+def test_single_rank_identity(dims):
+    """P = 1: identity for sum and avg (avg scales by exactly 1), every
+    entry point, loopback and the multi-process API."""
+    lb = ddl.Loopback(1, dims)
+    for dtype, op in _cases():
+        bufs = si.rank_buffers(dtype, KIND[dtype], 40_003, 1, seed=9)
+        want = oracle.allreduce(bufs, dims, dtype, op)
+        assert same_bits(want[0], bufs[0])
+        got = _run_lb(lb, bufs, dtype, op)
+        assert same_bits(got[0], want[0]), (dims, dtype, op)
+        dev = [[to_dev(bufs[0], dtype)]]
+        lb.all_reduce_many(dev, op)
+        torch.cuda.synchronize()
+        assert same_bits(to_host(dev[0][0]), want[0])
+        out = torch.empty(40_003, dtype=TORCH[dtype], device="cuda")
+        lb.reduce_scatter([out], [to_dev(bufs[0], dtype)], op)
+        torch.cuda.synchronize()
+        assert same_bits(to_host(out), want[0])
+    lb.finalize()
+    g = ddl.InProcessGroup(1, dims, max_bytes=1 << 20)
+    for algo in (ddl.ALGO_LL, ddl.ALGO_ONESHOT, ddl.ALGO_HIER, ddl.ALGO_AUTO):
+        g.set_algo(algo, 1 << 19)
+        for dtype, op in _cases():
+            bufs = si.rank_buffers(dtype, KIND[dtype], 3001, 1, seed=algo)
+            t = [to_dev(bufs[0], dtype)]
+            g.all_reduce(t, op)
+            torch.cuda.synchronize()
+            assert g.async_error() == ddl.SUCCESS
+            assert same_bits(to_host(t[0]), bufs[0]), (dims, algo, dtype, op)
+    g.finalize()
+
+
+@pytest.mark.parametrize("P,dims", [(8, [4, 1, 2]), (8, [1, 8]), (8, [8, 1]), (8, [2, 1, 2, 1, 2]), (4, [1, 2, 1, 2]),
+                                    (2, [1, 2])])
+def test_unit_dims_multiprocess_path(P, dims):
+    """The multi-process launch path (per-rank launches, .sys flags) with g_d = 1 dims:
+    LL, pull one-shot and hierarchical, zero-copy and staged, plus a grouped call."""
+    g = ddl.InProcessGroup(P, dims, max_bytes=16 << 20)
+    for algo in (ddl.ALGO_LL, ddl.ALGO_ONESHOT, ddl.ALGO_HIER):
+        g.set_algo(algo, 1 << 40 if algo == ddl.ALGO_ONESHOT else 0)
+        if algo == ddl.ALGO_LL:
+            g.set_ll_max(1 << 20)
+        for dtype, op in _cases():
+            for n in ((1, 33, 5000) if algo == ddl.ALGO_LL else (1, 1000, 300_001)):
+                bufs = si.rank_buffers(dtype, KIND[dtype], n, P, seed=n + algo)
+                want = oracle.allreduce(bufs, dims, dtype, op)
+                zc = [g.buffer(r, n, TORCH[dtype], offset_bytes=4096) for r in range(P)]
+                for r in range(P):
+                    zc[r].copy_(to_dev(bufs[r], dtype))
+                st = [to_dev(b, dtype) for b in bufs]
+                g.all_reduce(zc, op)
+                g.all_reduce(st, op)
+                torch.cuda.synchronize()
+                assert g.async_error() == ddl.SUCCESS
+                for r in range(P):
+                    for name, t in (("zero-copy", zc[r]), ("staged", st[r])):
+                        got = to_host(t)
+                        assert same_bits(got, want[r]), (name, dims, algo, dtype, op, n, r, first_diff(got, want[r]))
+    g.set_ll_max(64 << 10)
+    g.set_algo(ddl.ALGO_AUTO, 512 << 10)
+    sizes = [300_001, 700_003, 17, 150_000]
+    hosts = [si.rank_buffers("float32", "normal", n, P, seed=60 + i) for i, n in enumerate(sizes)]
+    offs, bk = 0, []
+    for n, hv in zip(sizes, hosts):
+        views = [g.buffer(r, n, torch.float32, offset_bytes=offs) for r in range(P)]
+        for r in range(P):
+            views[r].copy_(to_dev(hv[r], "float32"))
+        bk.append(views)
+        offs += (n * 4 + 255) // 256 * 256
+    g.all_reduce_many(bk, "avg")
+    torch.cuda.synchronize()
+    assert g.async_error() == ddl.SUCCESS
+    for hv, views in zip(hosts, bk):
+        w = oracle.allreduce(hv, dims, "float32", "avg")
+        for r in range(P):
+            assert same_bits(to_host(views[r]), w[r]), ("grouped", dims, r)
+    g.finalize()
+
+
+# ------------------------------------------------------------------ IEEE specials
+
+SPECIAL_DIMS = [(8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (2, [2]), (6, [3, 2])]
+
+
+def _specials(dtype, n, P, seed):
+    """'specials' draws plus columns where every rank holds a subnormal / signed zero (so
+    subnormal and -0 RESULTS occur at any P)."""
+    bufs = si.rank_buffers(dtype, "specials", n, P, seed=seed)
+    view = np.uint32 if dtype == "float32" else np.uint16
+    sub = [0x00000001, 0x80000001, 0x007FFFFF] if dtype == "float32" else [0x0001, 0x8001, 0x007F]
+    negz = 0x80000000 if dtype == "float32" else 0x8000
+    for r in range(P):
+        v = bufs[r].view(view)
+        for c in range(min(n, 24)):
+            v[c] = sub[(r + c) % 3] if c < 12 else (sub[0] if c < 16 else negz)
+    return bufs
+
+
+@pytest.mark.parametrize("P,dims", SPECIAL_DIMS, ids=[f"P{P}-{'x'.join(map(str, d))}" for P, d in SPECIAL_DIMS])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_ieee_specials_loopback(P, dims, dtype):
+    lb = ddl.Loopback(P, dims)
+    for algo in (ddl.ALGO_HIER, ddl.ALGO_ONESHOT):
+        lb.set_algo(algo, 1 << 40 if algo == ddl.ALGO_ONESHOT else 0)
+        for op in ("sum", "avg"):
+            for n in (24, 1000, 40_003, 300_001):
+                bufs = _specials(dtype, n, P, seed=n)
+                want = oracle.allreduce(bufs, dims, dtype, op)
+                got = _run_lb(lb, bufs, dtype, op)
+                for r in range(P):
+                    assert same_bits(got[r], want[r]), (dims, algo, dtype, op, n, r, first_diff(got[r], want[r]))
+    # grouped call with special-valued buckets
+    sizes = [300_001, 1_000_003, 5]
+    hosts = [_specials(dtype, n, P, seed=70 + i) for i, n in enumerate(sizes)]
+    devs = [[to_dev(h, dtype) for h in hv] for hv in hosts]
+    lb.set_algo(ddl.ALGO_AUTO, 512 << 10)
+    lb.all_reduce_many(devs, "avg")
+    torch.cuda.synchronize()
+    for hv, dv in zip(hosts, devs):
+        w = oracle.allreduce(hv, dims, dtype, "avg")
+        for r in range(P):
+            assert same_bits(to_host(dv[r]), w[r]), ("grouped", dims, dtype, r)
+    lb.finalize()
+
+
+def test_ieee_specials_local_reduce():
+    for dtype in ("float32", "bfloat16"):
+        for g in (2, 8):
+            ins = _specials(dtype, 100_003, g, seed=g)
+            for s in (1.0, 1.0 / g):
+                want = oracle.local_reduce(ins, dtype, s)
+                dev = [to_dev(x, dtype) for x in ins]
+                out = torch.empty_like(dev[0])
+                ddl.local_reduce(dev, out, s)
+                torch.cuda.synchronize()
+                got = to_host(out)
+                assert same_bits(got, want), (dtype, g, s, first_diff(got, want))
+
+
+@pytest.mark.parametrize("P,dims", [(8, [4, 2]), (4, [2, 2]), (2, [2])])
+def test_ieee_specials_multiprocess_path(P, dims):
+    g = ddl.InProcessGroup(P, dims, max_bytes=16 << 20)
+    for algo in (ddl.ALGO_LL, ddl.ALGO_ONESHOT, ddl.ALGO_HIER):
+        g.set_algo(algo, 1 << 40 if algo == ddl.ALGO_ONESHOT else 0)
+        if algo == ddl.ALGO_LL:
+            g.set_ll_max(1 << 20)
+        for dtype in ("float32", "bfloat16"):
+            for op in ("sum", "avg"):
+                for n in ((24, 5000) if algo == ddl.ALGO_LL else (1000, 300_001)):
+                    bufs = _specials(dtype, n, P, seed=n + algo)
+                    want = oracle.allreduce(bufs, dims, dtype, op)
+                    st = [to_dev(b, dtype) for b in bufs]
+                    g.all_reduce(st, op)
+                    torch.cuda.synchronize()
+                    assert g.async_error() == ddl.SUCCESS
+                    for r in range(P):
+                        got = to_host(st[r])
+                        assert same_bits(got, want[r]), (dims, algo, dtype, op, n, r, first_diff(got, want[r]))
+    g.finalize()
+
+
+# ------------------------------------------------------------------ the bench's exact call, full size
+
+def _sample_idx(n, k=4096, seed=0):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return np.unique(np.concatenate([rng.integers(0, n, k), np.arange(min(n, 64)), np.arange(max(0, n - 64), n)]))
+
+
+def _check_bucket_sampled(host_ranks, dev_ranks, dims, tag):
+    idx = _sample_idx(host_ranks[0].size, seed=host_ranks[0].size)
+    want = oracle.allreduce_sampled(host_ranks, dims, "float32", "avg", idx)
+    ti = torch.from_numpy(idx).to("cuda:0")
+    for r, t in enumerate(dev_ranks):
+        got = to_host(t[ti])
+        assert same_bits(got, want), (tag, r, first_diff(got, want))
+    for t in dev_ranks[1:]:
+        assert torch.equal(t.view(torch.int32), dev_ranks[0].view(torch.int32)), tag
+
+
+def test_bench_step_grouped_full_size_loopback():
+    """bench.py N = 1's exact step: Loopback(8, 2x4).all_reduce_many(5 ResNet-50 buckets,
+    avg) -- ddl_group_allreduce_many with the default channels -- twice (the second call on
+    the first's outputs, as in the bench's warm-up), every bucket vs the oracle."""
+    P, dims = 8, ddl.parse_dims("2x4")
+    lb = ddl.Loopback(P, dims, device=0)
+    nb = len(si.resnet50_bucket_bytes())
+    host = [[si.resnet50_bucket(b, r) for r in range(P)] for b in range(nb)]
+    bufs = [[to_dev(host[b][r], "float32") for r in range(P)] for b in range(nb)]
+    lb.all_reduce_many(bufs, "avg")
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    for b in range(nb):
+        _check_bucket_sampled(host[b], bufs[b], dims, f"bucket {b}")
+    # a second step on the reduced values (the bench repeats the step in place)
+    host2 = [[to_host(bufs[b][r]) for r in range(P)] for b in range(nb)]
+    lb.all_reduce_many(bufs, "avg")
+    torch.cuda.synchronize()
+    for b in range(nb):
+        _check_bucket_sampled(host2[b], bufs[b], dims, f"bucket {b} step 2")
+    lb.finalize()
+
+
+def test_bench_step_grouped_full_size_multiprocess_path():
+    """bench.py N > 1's step on the multi-process launch path: the 5 buckets in the symmetric
+    buffer (zero-copy), one ddl_allreduce_many per rank, 8 ranks 2x4, avg."""
+    P, dims = 8, ddl.parse_dims("2x4")
+    nb = len(si.resnet50_bucket_bytes())
+    host = [[si.resnet50_bucket(b, r) for r in range(P)] for b in range(nb)]
+    S = sum(h.size for h in (host[b][0] for b in range(nb))) * 4
+    g = ddl.InProcessGroup(P, dims, max_bytes=S + 256 * nb + (1 << 20))
+    offs, views = 0, []
+    for b in range(nb):
+        n = host[b][0].size
+        vb = [g.buffer(r, n, torch.float32, offs) for r in range(P)]
+        for r in range(P):
+            vb[r].copy_(torch.from_numpy(host[b][r]))
+        views.append(vb)
+        offs += (n * 4 + 255) // 256 * 256
+    g.all_reduce_many(views, "avg")
+    torch.cuda.synchronize()
+    assert g.async_error() == ddl.SUCCESS
+    for b in range(nb):
+        _check_bucket_sampled(host[b], views[b], dims, f"bucket {b}")
+    g.finalize()
+
+
+# ------------------------------------------------------------------ north_star's bf16 gate, every element
+
+@pytest.mark.parametrize("spec", ["8", "2x4", "4x2", "2x2x2"])
+def test_config4_bf16_gate_every_element(spec):
+    """BASELINE config 4 (bf16 256 MiB, avg, 8 ranks): north_star "bf16 within 1e-2" of an
+    fp64 naive sum, read componentwise as max_e |y - s/P| / (sum_r |x_r| / P) (ledger 8),
+    gated at exactly 1e-2 over all 134,217,728 elements; the measured maximum is printed
+    (DESIGN reading 7).  Bit-exactness vs the oracle is checked on sampled elements in
+    test_gpu_parity.py::test_config4_bf16_256MiB."""
+    P, dims = 8, ddl.parse_dims(spec)
+    n = (256 << 20) // 2
+    bufs = si.rank_buffers("bfloat16", "normal", n, P)
+    dev = [to_dev(x, "bfloat16") for x in bufs]
+    lb = ddl.Loopback(P, dims)
+    lb.all_reduce(dev, "avg")
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    # test-side fp64 reference on the device, in chunks (plain torch ops)
+    worst = 0.0
+    chunk = 1 << 24
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        s = torch.zeros(hi - lo, dtype=torch.float64, device="cuda")
+        a = torch.zeros_like(s)
+        for x in bufs:
+            xf = to_dev(x[lo:hi], "bfloat16").double()
+            s += xf
+            a += xf.abs()
+        y = dev[0][lo:hi].double()
+        err = ((y - s / P).abs() / (a / P).clamp_min(1e-300)).max().item()
+        worst = max(worst, err)
+    print(f"\nconfig4 bf16 {spec}: max |y - s/P| / (sum|x|/P) over {n} elements = {worst:.4e}")
+    assert worst <= 1e-2, worst
+    lb.finalize()
