@@ -40,7 +40,6 @@ import synthetic_inputs as si  # noqa: E402
 
 METRIC = "allreduce bus GB/s vs msg size at 2/4/8 B200 (% of 900 GB/s NVLink) vs NCCL"
 NVLINK_NOMINAL = 900.0
-NVLINK_MEASURED_PEER = 770.0   # B200_PROFILING.md: measured peer copy per direction
 DIMS_FOR_N = {1: "2x4", 2: "2", 4: "2x2", 8: "2x4"}
 
 
@@ -205,6 +204,50 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- value gate
+def value_gate(lb, sizes, P, dims, dev, bufs):
+    """Before any timing, the exact step call is checked on VALUES, not only on agreement
+    between ranks (a schedule that drops or doubles one rank the same way everywhere would
+    still agree):
+      1. closed forms through the grouped call on the step's bucket sizes: fp32 x_r = r + 1
+         with avg gives (P+1)/2 exactly; int32 x_r[i] = (1<<r) | ((i mod 2^20) << 8) with
+         sum gives (2^P - 1) + P * ((i mod 2^20) << 8) mod 2^32 (a missing / doubled rank
+         shows in the low byte, a misplaced element in the high bits);
+      2. the grouped step on the real gradient set equals the 5 single calls bit for bit
+         (the single calls are the path tests/ check element by element against the oracle).
+    Restores the buffers to the step's inputs afterwards."""
+    import torch
+    # 1a. fp32 r+1, avg
+    ones = [[torch.full((n,), float(r + 1), device=dev) for r in range(P)] for n in sizes]
+    lb.all_reduce_many(ones, "avg")
+    # 1b. int32 bitmask, sum
+    mask = []
+    for n in sizes:
+        i = torch.arange(n, device=dev, dtype=torch.int64)
+        mask.append([(((i % (1 << 20)) << 8) | (1 << r)).to(torch.int32) for r in range(P)])
+    lb.all_reduce_many(mask, "sum")
+    torch.cuda.synchronize()
+    for b, n in enumerate(sizes):
+        assert all(bool((t == (P + 1) / 2).all()) for t in ones[b]), f"closed form r+1 avg failed, bucket {b}"
+        i = torch.arange(n, device=dev, dtype=torch.int64)
+        want = ((((1 << P) - 1) + P * ((i % (1 << 20)) << 8)) & 0xFFFFFFFF)
+        want = torch.where(want >= (1 << 31), want - (1 << 32), want).to(torch.int32)
+        assert all(torch.equal(t, want) for t in mask[b]), f"closed form bitmask failed, bucket {b}"
+    del ones, mask
+    # 2. grouped == single calls, on copies of the step's inputs
+    a = [[t.clone() for t in bk] for bk in bufs]
+    s_ = [[t.clone() for t in bk] for bk in bufs]
+    lb.all_reduce_many(a, "avg")
+    for bk in s_:
+        lb.all_reduce(bk, "avg")
+    torch.cuda.synchronize()
+    for b in range(len(sizes)):
+        assert all(torch.equal(x.view(torch.int32), y.view(torch.int32)) for x, y in zip(a[b], s_[b])), \
+            f"grouped != single calls, bucket {b}"
+    return ("closed forms (fp32 r+1 avg, int32 bitmask sum) through the grouped call on the step's bucket "
+            "sizes; grouped step == 5 single calls bitwise; all ranks identical after warm-up")
+
+
 # ----------------------------------------------------------------------------- N = 1: loopback
 def run_loopback(args):
     import torch
@@ -236,6 +279,7 @@ def run_loopback(args):
             if evs is not None:
                 evs[b][1].record(stream)
 
+    gate = value_gate(lb, sizes, P, dims, dev, bufs)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:   # sampling spans warm-up + timed region (>= a few 100-ms samples)
         for _ in range(args.warmup):
@@ -381,6 +425,7 @@ def run_loopback(args):
                        "ddl_group_allreduce || D2H of the reduced bucket (PCIe-bound)"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
+        "correctness_gate": gate,
         "local_reduce": {"g": g, "bytes": (g + 1) * n5 * 4, "ms": k5_ms, "achieved": k5_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": k5_gbs / hbm_peak},
     }
@@ -391,6 +436,33 @@ def run_loopback(args):
 
 
 # ----------------------------------------------------------------------------- N > 1
+def peer_copy_gbs(comm, P, rank, nbytes, offset, reps=10):
+    """Peer-copy peak measured in the same run: every rank copies nbytes from its own
+    symmetric buffer into rank (r+1) mod P's (mapped over NVLink), all ranks at once
+    (cudaMemcpyAsync on UVA peer pointers = the copy engines), so each GPU sends and
+    receives one stream: GB/s per direction per GPU, max time over ranks."""
+    import torch
+    import torch.distributed as dist
+    n = nbytes // 4
+    src = comm.buffer(n, torch.float32, offset)
+    dst = comm.peer_buffer((rank + 1) % P, n, torch.float32, offset + (nbytes + 255) // 256 * 256)
+    stream = torch.cuda.current_stream()
+    for _ in range(2):
+        dst.copy_(src)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        dst.copy_(src)
+    b.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / reps], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    return nbytes / (t.item() * 1e-3) / 1e9
+
+
 def run_multi(args):
     import torch
     import torch.distributed as dist
@@ -411,7 +483,9 @@ def run_multi(args):
     host = resnet50_set(rank)
     sizes = [h.size for h in host]
     S_total = sum(sizes) * 4
-    comm = ddl.init(dims, max_bytes=S_total + 256 * len(sizes) + (1 << 20))
+    copy_bytes = 64 << 20
+    sym_bytes = (S_total + 256 * len(sizes) + 255) // 256 * 256
+    comm = ddl.init(dims, max_bytes=sym_bytes + 2 * copy_bytes + (1 << 20))
     offs, views = 0, []
     for h in host:                                   # buckets live in the symmetric buffer (zero-copy)
         v = comm.buffer(h.size, torch.float32, offs)
@@ -419,6 +493,7 @@ def run_multi(args):
         views.append(v)
         offs += (h.size * 4 + 255) // 256 * 256
     stream = torch.cuda.current_stream()
+    cuda_or_cpu = "cpu" if same_gpu else "cuda"
 
     def step():   # the 5 buckets in one grouped all-reduce (as at N = 1)
         comm.all_reduce_many(views, "avg")
@@ -442,13 +517,42 @@ def run_multi(args):
             evs.append((a, b))
         torch.cuda.synchronize()
         dist.barrier()
-        t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / steps], device="cpu" if same_gpu else "cuda")
+        t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / steps], device=cuda_or_cpu)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)   # max over ranks
         return t.item()
 
+    # correctness gate on values before any timing: closed forms through the grouped call
+    # (fp32 r+1 avg -> (P+1)/2 exactly; int32 bitmask sum -> (2^P-1) + P*((i mod 2^20)<<8))
+    gate_ok = True
+    for kind in ("r+1", "bitmask"):
+        o2, tv = 0, []
+        for n in sizes:
+            t = comm.buffer(n, torch.float32 if kind == "r+1" else torch.int32, o2)
+            if kind == "r+1":
+                t.fill_(float(rank + 1))
+            else:
+                i = torch.arange(n, device=f"cuda:{dev_idx}", dtype=torch.int64)
+                t.copy_((((i % (1 << 20)) << 8) | (1 << rank)).to(torch.int32))
+            tv.append(t)
+            o2 += (n * 4 + 255) // 256 * 256
+        comm.all_reduce_many(tv, "avg" if kind == "r+1" else "sum")
+        torch.cuda.synchronize()
+        for t, n in zip(tv, sizes):
+            if kind == "r+1":
+                gate_ok &= bool((t == (P + 1) / 2).all())
+            else:
+                i = torch.arange(n, device=f"cuda:{dev_idx}", dtype=torch.int64)
+                w_ = (((1 << P) - 1) + P * ((i % (1 << 20)) << 8)) & 0xFFFFFFFF
+                gate_ok &= torch.equal(t, torch.where(w_ >= (1 << 31), w_ - (1 << 32), w_).to(torch.int32))
+    okt = torch.tensor([0 if gate_ok else 1], device=cuda_or_cpu)
+    dist.all_reduce(okt, op=dist.ReduceOp.MAX)
+    assert okt.item() == 0, "closed-form gate failed on some rank"
+    for v, h in zip(views, host):                     # restore the gradient set
+        v.copy_(torch.from_numpy(h))
+
     for _ in range(args.warmup):
         step()
-    # correctness gate before timing: every rank holds bit-identical results
+    # all ranks bit-identical after the warm-up steps
     digest = torch.tensor([int(v.view(torch.int32).to(torch.int64).sum().item()) for v in views], dtype=torch.int64)
     alld = [torch.zeros_like(digest) for _ in range(world)]
     dist.all_gather(alld, digest.cuda() if not same_gpu else digest)
@@ -460,16 +564,48 @@ def run_multi(args):
     singles = sum(1 for s in sizes if comm.algo_for(s, "float32") != ddl.ALGO_HIER)
     launches = singles + -(-(len(sizes) - singles) // 8)
 
-    nccl_ms = None
+    # per-bucket bus bandwidth: each bucket as one single call (events per call, max over ranks)
+    per_bucket = []
+    for v, n in zip(views, sizes):
+        tb = timed(lambda v=v: comm.all_reduce(v, "avg"), max(3, min(args.steps, 20)))
+        per_bucket.append({"bytes": n * 4, "us": round(tb * 1e3, 2),
+                           "busbw": round(n * 4 * 2 * (P - 1) / P / (tb * 1e-3) / 1e9, 1)})
+
+    # peer-copy peak of this box, measured now (the roofline's measured denominator)
+    peer_gbs = peer_copy_gbs(comm, P, rank, copy_bytes, sym_bytes)
+
+    nccl = None
     if not same_gpu:
+        nccl = {"version": ".".join(map(str, torch.cuda.nccl.version()))}
         nccl_bufs = [torch.from_numpy(h).cuda() for h in host]
 
-        def nccl_step():
+        def nccl_step(group=None):
             for t in nccl_bufs:
-                dist.all_reduce(t, op=dist.ReduceOp.AVG)
+                dist.all_reduce(t, op=dist.ReduceOp.AVG, group=group)
         for _ in range(args.warmup):
             nccl_step()
         nccl_ms = timed(nccl_step, args.steps)
+        nccl["default"] = {"value": S_total * 2 * (P - 1) / P / (nccl_ms * 1e-3) / 1e9, "unit": "GB/s",
+                           "ms_per_step": nccl_ms}
+        # NCCL with its NVLS (NVSwitch multicast) algorithms excluded: a second communicator
+        # created while NCCL_ALGO excludes them (NCCL reads NCCL_ALGO at communicator init;
+        # NCCL_NVLS_ENABLE is cached per process, so it cannot be toggled here)
+        old = os.environ.get("NCCL_ALGO")
+        try:
+            os.environ["NCCL_ALGO"] = "^NVLS,NVLSTree"
+            g2 = dist.new_group(list(range(world)))
+            for _ in range(args.warmup):
+                nccl_step(g2)
+            t2 = timed(lambda: nccl_step(g2), args.steps)
+            nccl["no_nvls"] = {"value": S_total * 2 * (P - 1) / P / (t2 * 1e-3) / 1e9, "unit": "GB/s",
+                               "ms_per_step": t2, "how": "NCCL_ALGO=^NVLS,NVLSTree on a second communicator"}
+        except Exception as e:   # record, never fail the bench line on the comparison
+            nccl["no_nvls"] = {"error": repr(e)[:200]}
+        finally:
+            if old is None:
+                os.environ.pop("NCCL_ALGO", None)
+            else:
+                os.environ["NCCL_ALGO"] = old
 
     # e2e: host gradients -> device (pinned H2D), all-reduce, reduced gradients -> host
     pinned = [torch.from_numpy(h).pin_memory() for h in host]
@@ -491,6 +627,12 @@ def run_multi(args):
     e2e_step()
     e2e_ms = timed(e2e_step, max(3, min(args.steps, 10)), flush=False)   # fresh H2D data every step
 
+    # the oracle on the same per-rank set at P simulated ranks (rank 0 only, bounded)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = oracle_baseline(P, dims, [resnet50_set(r) for r in range(P)])
+    dist.barrier()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": busbw, "unit": "GB/s", "n_gpus": P, "steps": args.steps,
@@ -499,23 +641,36 @@ def run_multi(args):
             "config": {"workload": f"resnet50-grad-set all-reduce avg, {P} ranks (1 per GPU), dims "
                                    + "x".join(map(str, dims[::-1])),
                        "dims": "x".join(map(str, dims[::-1])), "n_ranks": P, "bytes_per_rank": S_total,
-                       "buckets": sizes,
+                       "buckets": sizes, "same_gpu": same_gpu,
+                       "step": "one grouped all-reduce of the 5 buckets (ddl_allreduce_many, zero-copy buffers)",
                        "l2": "flushed between timed steps (256 MiB write per rank, outside the per-step events)"},
-            "roofline": {"bound": "nvlink", "achieved": busbw, "peak": NVLINK_MEASURED_PEER,
-                         "unit": "GB/s", "frac": busbw / NVLINK_MEASURED_PEER, "traffic": None,
-                         "frac_of_nominal_900": busbw / NVLINK_NOMINAL,
-                         "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)"},
-            "nccl": None if nccl_ms is None else {"value": S_total * 2 * (P - 1) / P / (nccl_ms * 1e-3) / 1e9,
-                                                  "unit": "GB/s", "ms_per_step": nccl_ms},
+            # roofline: NVLink per direction per GPU; algorithmic bytes 2S(P-1)/P for every
+            # factorisation, so `achieved` = the bus bandwidth
+            "roofline": {"bound": "nvlink", "achieved": busbw, "peak": NVLINK_NOMINAL, "unit": "GB/s",
+                         "frac": busbw / NVLINK_NOMINAL,
+                         "peak_source": "north_star: 900 GB/s per direction per GPU (NVLink 5 nominal)",
+                         "measured_peer_copy": peer_gbs,
+                         "frac_of_measured_peer_copy": busbw / peer_gbs if peer_gbs else None,
+                         "peer_copy_how": f"all ranks at once, {copy_bytes} B own buffer -> rank+1's "
+                                          "(cudaMemcpyAsync over the cudaIpc mapping), max over ranks",
+                         "algorithmic_bytes_per_step": int(S_total * 2 * (P - 1) / P),
+                         "traffic": None,
+                         "traffic_how": "NVLink bytes need ncu with --replay-mode application on every rank: "
+                                        "scripts/ncu_nvlink.sh"},
+            "per_bucket": per_bucket,
+            "nccl": nccl,
             "e2e": {"value": S_total * 2 * (P - 1) / P / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": S_total, "d2h_bytes_per_step": S_total},
             "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
+            "correctness_gate": "closed forms (fp32 r+1 avg, int32 bitmask sum) through the grouped call on "
+                                "the step's bucket sizes, every rank; all ranks identical after warm-up",
         }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     comm.finalize()
     dist.destroy_process_group()
-
 
 
 def main():

@@ -35,7 +35,12 @@
  *     communicator must be ordered (one stream, or externally serialised): the device
  *     barriers of consecutive calls are told apart by a per-rank call counter.
  *   - Calls are CUDA-graph capturable: all per-call state (the call counter, the flags)
- *     lives in device memory.
+ *     lives in device memory.  One exception: ddl_group_reduce_scatter grows its loopback
+ *     workspace on demand, which cannot happen inside a capture -- a captured call that
+ *     would need a larger workspace returns DDL_ERR_TOO_LARGE (make one uncaptured call
+ *     of the largest size first).
+ *   - Calls whose per-CTA slice would reach 1 GiB (only with DDL_CTAS forced tiny and
+ *     multi-GiB messages) are cut into waves, or return DDL_ERR_TOO_LARGE.
  *   - The caller owns buffers, streams and the comm handle; the library owns its
  *     workspace, flags and IPC mappings and releases them in ddl_finalize().  No C++
  *     exception crosses the ABI and the library never aborts the process.
@@ -127,6 +132,11 @@ ddl_result_t ddl_connect(ddl_comm_t comm, const void* all_handles /* nranks * ha
 /* The symmetric zero-copy buffer (max_bytes, 256-B aligned).  An all-reduce on a buffer
  * inside it, at the SAME offset on every rank, reads peers' data in place (no staging). */
 ddl_result_t ddl_buffer(ddl_comm_t comm, void** dev_ptr, size_t* bytes);
+/* Rank `peer`'s symmetric buffer as mapped into this process (cudaIpc over NVLink; this
+ * rank's own buffer for peer == rank).  For measurement and diagnostics (bench.py's
+ * peer-copy peak); writing into it races with the peer's collectives unless the caller
+ * orders them.  DDL_ERR_NOT_CONNECTED before ddl_connect. */
+ddl_result_t ddl_peer_buffer(ddl_comm_t comm, int peer, void** dev_ptr, size_t* bytes);
 
 /* Registered buffers (SURVEY 8(b) ddl_register): persistent user buffers -- e.g. DDP's
  * gradient buckets -- made zero-copy.  Collective: every rank calls
@@ -151,8 +161,9 @@ ddl_result_t ddl_allreduce(ddl_comm_t comm, void* buf, size_t count, ddl_dtype_t
  * one SGD step) in as few launches as possible.  bufs[i] holds counts[i]
  * elements (16-B aligned, not overlapping one another; counts[i] == 0 is skipped); every
  * rank passes the same nbufs and counts in the same order.  Buffers in the LL / one-shot size regime, staged (not
- * symmetric / registered) buffers, and every buffer under DDL_CHECK are all-reduced first
- * by single ddl_allreduce calls, in order; the remaining zero-copy buffers share one launch
+ * symmetric / registered) buffers, and every buffer under DDL_CHECK or a non-default
+ * phase kernel (DDL_NO_TMA register-staged fallback, DDL_STEAL / DDL_DYN / DDL_STREAM
+ * experiments) are all-reduced first by single ddl_allreduce calls, in order; the remaining zero-copy buffers share one launch
  * per 8 buffers, split over DDL_CHANNELS (default 2) channels of CTAs that each run their
  * buffers' hierarchical schedules one after another, so that one channel's barrier waits
  * and L2-bound phases overlap another's HBM / NVLink-bound phases.  Results are
@@ -238,7 +249,8 @@ ddl_result_t ddl_group_allreduce(ddl_comm_t comm, void* const* bufs, size_t coun
 ddl_result_t ddl_group_allreduce_many(ddl_comm_t comm, void* const* bufs, const size_t* counts, int nbufs,
                                       ddl_dtype_t dtype, ddl_op_t op, void* stream);
 /* sendbufs[r]: nranks*recvcount elements (not modified); recvbufs[r]: recvcount.
- * Uses a library workspace of nranks * nranks * recvcount elements (grown on demand). */
+ * Uses a library workspace of nranks * nranks * recvcount elements (grown on demand;
+ * DDL_ERR_TOO_LARGE if it must grow while the stream is being captured). */
 ddl_result_t ddl_group_reduce_scatter(ddl_comm_t comm, const void* const* sendbufs, void* const* recvbufs,
                                       size_t recvcount, ddl_dtype_t dtype, ddl_op_t op, void* stream);
 /* sendbufs[r]: sendcount elements; recvbufs[r]: nranks*sendcount elements. */

@@ -304,6 +304,12 @@ ddl_result_t common_init(ddl_comm* c, int nranks, const int* dims, int ndims, in
 }
 
 // ---------------------------------------------------------------- per-call plan
+// UnitDesc::bytes and the register-staged item prefixes are 32-bit: one CTA's slice of a
+// block must stay below this many bytes (reached only with DDL_CTAS tiny and multi-GiB
+// messages).  Larger slices are cut into waves where the kernel has them, else the call
+// returns DDL_ERR_TOO_LARGE -- never a silent wrap.
+constexpr uint64_t kMaxSliceBytes = 1ull << 30;
+
 struct Plan {
   uint64_t q = 0;
   uint64_t slice = 0;
@@ -408,6 +414,8 @@ Plan plan_hier(const ddl_comm* c, uint64_t n, uint64_t q, ddl_dtype_t dt, bool v
     const uint64_t sb = pl.slice * (uint64_t)w;
     waves = (c->gpu_share == c->P) ? (int)std::min<uint64_t>(32, sb / c->wave_slice_bytes) : 1;
   }
+  if (pl.path == 2 && pl.slice * (uint64_t)w > kMaxSliceBytes)  // 32-bit slice fields: cut into waves
+    waves = std::max<int>(waves, (int)((pl.slice * (uint64_t)w + kMaxSliceBytes - 1) / kMaxSliceBytes));
   if (waves > 1 && pl.path == 2) {
     uint64_t s2 = (q + (uint64_t)pl.nctas * waves - 1) / ((uint64_t)pl.nctas * waves);
     s2 = (s2 + W - 1) / W * W;
@@ -510,6 +518,7 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
                    : pl.oneshot ? oneshot_fn_dt(dt, c->topo.nlive, pl.r)
                                 : hier_fn_dt(dt, pl.path);
   if (!fn) return DDL_ERR_UNSUPPORTED;
+  if (!pl.oneshot && !pl.ll && pl.slice * (uint64_t)elem_size(dt) > kMaxSliceBytes) return DDL_ERR_TOO_LARGE;
   p.nwaves = (pl.oneshot || pl.ll) ? 1 : pl.nwaves;
   const size_t smem = (pl.oneshot || pl.ll) ? 0 : hier_smem(pl.path);
   blocks_per_sm(fn, smem);  // sets the dynamic shared-memory attribute once
@@ -753,6 +762,14 @@ ddl_result_t ddl_connect(ddl_comm_t c, const void* all_handles) {
     c->peer_mapped[m] = true;
   }
   c->connected = true;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_peer_buffer(ddl_comm_t c, int peer, void** dev_ptr, size_t* bytes) {
+  if (!c || !dev_ptr || !bytes || c->loopback || peer < 0 || peer >= c->P) return DDL_ERR_INVALID_ARGUMENT;
+  if (peer != c->rank && !c->peer_mapped[peer]) return DDL_ERR_NOT_CONNECTED;
+  *dev_ptr = c->sym_of(peer);
+  *bytes = c->max_bytes;
   return DDL_SUCCESS;
 }
 
@@ -1139,6 +1156,13 @@ static const void* multi_fn_dt(ddl_dtype_t dt) {
 // buffer ptrs[i * P + m] (hierarchical-sized, 16-B aligned, zero-copy), at most kMaxBuckets
 // per launch.  Buckets go to channels longest-first onto the least-loaded channel; each
 // channel gets CTAs in proportion to its bytes and runs its buckets in their given order.
+// The grouped kernel runs the TMA-staged phases only.  With DDL_NO_TMA (the register-staged
+// fallback should bulk copies from peer memory fail) or an experimental variant selected,
+// every bucket goes through a single call instead, so the variant choice holds everywhere.
+static bool grouped_kernel_ok(const ddl_comm* c) {
+  return c->use_tma && !c->use_dyn && !c->use_steal && !c->use_stream;
+}
+
 static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* const* ptrs, int nb, ddl_dtype_t dt,
                                  ddl_op_t op, void* stream) {
   const void* fn = multi_fn_dt(dt);
@@ -1216,6 +1240,8 @@ static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* co
       // other channels stream.
       int gw = c->group_waves;
       if (gw == 0) gw = (int)std::min<uint64_t>(32, (slice * w + c->wave_slice_bytes / 2) / c->wave_slice_bytes);
+      if (slice * w > kMaxSliceBytes)  // 32-bit slice fields: cut into waves
+        gw = std::max<int>(gw, (int)((slice * w + kMaxSliceBytes - 1) / kMaxSliceBytes));
       if (gw > 1) {
         uint64_t s2 = (q + (uint64_t)nc * gw - 1) / ((uint64_t)nc * gw);
         s2 = (s2 + W - 1) / W * W;
@@ -1224,6 +1250,7 @@ static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* co
           nw = (int)((q + (uint64_t)nc * s2 - 1) / ((uint64_t)nc * s2));
         }
       }
+      if (slice * w > kMaxSliceBytes) return DDL_ERR_TOO_LARGE;
       waves_of[i] = nw;
       mp.b[i].n = n;
       mp.b[i].q = q;
@@ -1299,7 +1326,7 @@ ddl_result_t ddl_group_allreduce_many(ddl_comm_t c, void* const* bufs, const siz
   for (int i = 0; i < nbufs; ++i) {
     if (!counts[i]) continue;
     Plan pl;
-    if (use_oneshot(c, counts[i], dt, &pl)) {
+    if (!grouped_kernel_ok(c) || use_oneshot(c, counts[i], dt, &pl)) {
       if ((r = ddl_group_allreduce(c, bufs + (size_t)i * c->P, counts[i], dt, op, stream)) != DDL_SUCCESS) return r;
       continue;
     }
@@ -1327,7 +1354,8 @@ ddl_result_t ddl_allreduce_many(ddl_comm_t c, void* const* bufs, const size_t* c
     if (!counts[i]) continue;
     const char* peer[kMaxRanks];
     Plan pl;
-    const bool single = c->check || use_ll(c, counts[i], dt, &pl) || use_oneshot(c, counts[i], dt, &pl) ||
+    const bool single = c->check || !grouped_kernel_ok(c) || use_ll(c, counts[i], dt, &pl) ||
+                        use_oneshot(c, counts[i], dt, &pl) ||
                         !zero_copy_peers(c, bufs[i], counts[i] * elem_size(dt), peer);
     if (single) {
       if ((r = ddl_allreduce(c, bufs[i], counts[i], dt, op, stream)) != DDL_SUCCESS) return r;
@@ -1377,6 +1405,10 @@ ddl_result_t ddl_group_reduce_scatter(ddl_comm_t c, const void* const* sendbufs,
   DDL_ON_DEVICE(c->device);
   const size_t need = (n * w + 255) / 256 * 256;
   if (need > c->lb_ws_bytes) {
+    // growing the workspace synchronises and reallocates: not allowed inside stream capture
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    DDL_CUDA(cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cap));
+    if (cap != cudaStreamCaptureStatusNone) return DDL_ERR_TOO_LARGE;
     DDL_CUDA(cudaDeviceSynchronize());
     if (c->lb_ws) cudaFree(c->lb_ws);
     c->lb_ws = nullptr;

@@ -66,6 +66,7 @@ def _load() -> ctypes.CDLL:
         "ddl_export_handle": (c_int, [c_void, c_void]),
         "ddl_connect": (c_int, [c_void, c_void]),
         "ddl_buffer": (c_int, [c_void, pp, ctypes.POINTER(c_size)]),
+        "ddl_peer_buffer": (c_int, [c_void, c_int, pp, ctypes.POINTER(c_size)]),
         "ddl_allreduce": (c_int, [c_void, c_void, c_size, c_int, c_int, c_void]),
         "ddl_allreduce_many": (c_int, [c_void, pp, ctypes.POINTER(c_size), c_int, c_int, c_int, c_void]),
         "ddl_reduce_scatter": (c_int, [c_void, c_void, c_void, c_size, c_int, c_int, c_void]),
@@ -268,6 +269,19 @@ class Comm:
         if offset_bytes % 256 or offset_bytes + count * esz > self.buffer_bytes:
             raise DDLError(ERR_TOO_LARGE, "view outside the symmetric buffer")
         full = _tensor_from_ptr(self.buffer_ptr, self.buffer_bytes, self.device)
+        return full[offset_bytes:offset_bytes + count * esz].view(dtype)
+
+    def peer_buffer(self, peer: int, count: int, dtype, offset_bytes: int = 0):
+        """A tensor view of rank ``peer``'s symmetric buffer as mapped here (over NVLink);
+        for measurement only (bench.py's peer-copy peak)."""
+        torch = _torch()
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _check(_lib.ddl_peer_buffer(self.h, peer, ctypes.byref(p), ctypes.byref(n)), "ddl_peer_buffer")
+        esz = torch.tensor([], dtype=dtype).element_size()
+        if offset_bytes + count * esz > n.value:
+            raise DDLError(ERR_TOO_LARGE, "view outside the peer's symmetric buffer")
+        full = _tensor_from_ptr(p.value, n.value, self.device)
         return full[offset_bytes:offset_bytes + count * esz].view(dtype)
 
     def all_reduce(self, t, op: str = "sum", stream=None):

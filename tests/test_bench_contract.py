@@ -6,6 +6,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 import bench
 from paper_1811_12174_b200 import ddl
 
@@ -65,3 +67,32 @@ def test_loopback_algorithmic_bytes_match_planner_traffic():
                             mb = sum(blen(b) for b in ddl.plan_blocks(P, dims, m, d + 1))
                             want += 2 * mb
             assert got == want, (dims, n, got, want)
+
+
+N_GT_1_KEYS = ("roofline", "cpu_baseline", "e2e", "nccl", "per_bucket", "clocks", "gpu_launches",
+               "correctness_gate")
+
+
+@pytest.mark.gpu
+def test_multi_rank_line_same_gpu():
+    """The N > 1 leg (torchrun, one process per rank) produces a complete line: roofline
+    (900 GB/s peak + a peer-copy peak measured in the run), cpu_baseline, e2e, nccl (null on
+    one GPU: NCCL refuses two ranks per device), per-bucket bus bandwidth.  Run with every
+    rank on cuda:0 (DDL_BENCH_SAME_GPU=1) -- a functional check; the numbers mean nothing."""
+    env = dict(os.environ, DDL_BENCH_SAME_GPU="1", DDL_TIMEOUT_MS="60000")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29631", os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    for k in REQUIRED + N_GT_1_KEYS:
+        assert k in d, k
+    assert d["n_gpus"] == 2 and d["config"]["same_gpu"] is True
+    assert d["roofline"]["peak"] == 900.0 and d["roofline"]["measured_peer_copy"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+    assert d["nccl"] is None
+    assert len(d["per_bucket"]) == 5 and all(b["busbw"] > 0 for b in d["per_bucket"])
+    assert d["e2e"]["h2d_bytes_per_step"] > 0

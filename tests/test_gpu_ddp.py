@@ -57,7 +57,7 @@ def _rank_main(rank, world, port, q):
             opt.step()
         torch.cuda.synchronize()
         params = [p.detach().cpu().numpy() for p in model.module.parameters()]  # by value
-        nreg = len(comm._ddp_registered)
+        nreg = len(comm._ddp_hook["regs"])
         # a rebuilt bucket (same index, new buffer): the old registration is dropped, the new
         # buffer registered and reduced zero-copy -- the registration count does not grow
         class _Bucket:
@@ -70,9 +70,15 @@ def _rank_main(rank, world, port, q):
             def index(self):
                 return self.i
         nb = torch.full((5000,), float(rank + 1), device="cuda")
+        late = False
+        try:            # past the agreement window a changed buffer raises (never a hang)
+            ddl_allreduce_hook(comm, _Bucket(nb, 0)).wait()
+        except RuntimeError:
+            late = True
+        comm._ddp_hook["calls"].clear()        # a rebuild inside the agreement window
         ddl_allreduce_hook(comm, _Bucket(nb, 0)).wait()
         torch.cuda.synchronize()
-        rebuilt_ok = bool((nb == (world + 1) / 2).all()) and len(comm._ddp_registered) == nreg
+        rebuilt_ok = late and bool((nb == (world + 1) / 2).all()) and len(comm._ddp_hook["regs"]) == nreg
         q.put((rank, params, comm.async_error() if rebuilt_ok else -2))
         comm.finalize()
     except Exception as e:

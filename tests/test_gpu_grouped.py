@@ -171,3 +171,71 @@ def test_loopback_grouped_tiny_buckets_forced_hierarchical(dtype):
     assert lb.async_error() == ddl.SUCCESS
     check_buckets(devs, hosts, dims, dtype, op, "tiny")
     lb.finalize()
+
+
+@pytest.mark.parametrize("env", [{"DDL_NO_TMA": "1"}, {"DDL_STREAM": "1"}, {"DDL_STEAL": "1"}],
+                         ids=["no-tma", "stream", "steal"])
+def test_grouped_honours_kernel_variant(env):
+    """DDL_NO_TMA=1 (the register-staged fallback if bulk copies from peer memory fail) and
+    the experimental variants hold for all_reduce_many too: every bucket goes through a
+    single call of the selected kernel (the grouped kernel is TMA-only), on the
+    loopback and the multi-process launch paths, bit-exact vs the oracle."""
+    P, dims = 8, [4, 2]
+    lb = with_env(env, lambda: ddl.Loopback(P, dims))
+    hosts, devs = make(P, "float32", SIZES, seed=500)
+    lb.all_reduce_many(devs, "avg")
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    check_buckets(devs, hosts, dims, "float32", "avg", f"loopback {env}")
+    lb.finalize()
+    g = with_env(dict(env, DDL_TIMEOUT_MS="5000"), lambda: ddl.InProcessGroup(4, [2, 2], max_bytes=32 << 20))
+    sizes = [700_001, 1_300_000, 300_000]
+    hosts = [si.rank_buffers("bfloat16", "normal", n, 4, seed=600 + i) for i, n in enumerate(sizes)]
+    bufs, off = [], 0
+    for hv in hosts:
+        n = hv[0].size
+        views = [g.buffer(r, n, torch.bfloat16, off) for r in range(4)]
+        for r in range(4):
+            views[r].copy_(to_dev(hv[r], "bfloat16"))
+        bufs.append(views)
+        off += (n * 2 + 255) // 256 * 256
+    g.all_reduce_many(bufs, "avg")
+    torch.cuda.synchronize()
+    assert g.async_error() == ddl.SUCCESS
+    check_buckets(bufs, hosts, [2, 2], "bfloat16", "avg", f"inproc {env}")
+    g.finalize()
+
+
+def test_reduce_scatter_workspace_growth_refused_in_capture():
+    """ddl_group_reduce_scatter grows its workspace on demand; inside a stream
+    capture that must be refused (DDL_ERR_TOO_LARGE), not break the capture; after an
+    uncaptured call of the size, the captured call works and replays bit-exact."""
+    P, dims, recv = 4, [2, 2], 300_000
+    lb = ddl.Loopback(P, dims)
+    sends = [torch.zeros(P * recv, device="cuda") for _ in range(P)]
+    outs = [torch.empty(recv, device="cuda") for _ in range(P)]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(ddl.DDLError) as ei:
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                lb.reduce_scatter(outs, sends)
+    assert ei.value.code == ddl.ERR_TOO_LARGE
+    torch.cuda.synchronize()
+    lb.reduce_scatter(outs, sends)          # grows the workspace outside a capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            lb.reduce_scatter(outs, sends, "avg")
+    torch.cuda.synchronize()
+    bufs = si.rank_buffers("float32", "normal", P * recv, P, seed=8)
+    for r in range(P):
+        sends[r].copy_(to_dev(bufs[r], "float32"))
+    g.replay()
+    torch.cuda.synchronize()
+    want = oracle.reduce_scatter(bufs, dims, "float32", "avg")
+    for r in range(P):
+        assert same_bits(to_host(outs[r]), want[r]), r
+    lb.finalize()
