@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__(kThreads, 1) ddl_ll_kernel(const __grid_consta
   using A = typename Tr<T>::Acc;
   constexpr int NE = 8 / (int)sizeof(T);  // elements per 8 data bytes
   constexpr int CH = 8;
-  const int me = p.rank;
+  const int me = p.loopback ? (int)blockIdx.y : p.rank;  // loopback: grid (ctas, P), co-resident
   const uint32_t e = rank_epoch_begin(p, me);
   if (me == p.skip_rank) return;
   const Topo& t = p.t;

@@ -131,6 +131,7 @@ struct ddl_comm {
   char* lb_flags = nullptr;
   char* lb_ws = nullptr;
   size_t lb_ws_bytes = 0;  // per virtual rank
+  char* lb_ll = nullptr;   // loopback LL receive regions: P x (two halves of P slots of ll_slot bytes)
   int* err = nullptr;      // sticky device error
   ddl_algo_t algo = DDL_ALGO_AUTO;
   size_t oneshot_max = 512 << 10;  // crossover measured in loopback (profiles/r01_oneshot_crossover.txt)
@@ -187,7 +188,10 @@ struct ddl_comm {
   // LL receive region after the scratch: two halves of P slots of ll_slot bytes
   size_t ll_max = 64 << 10;  // AUTO uses LL up to this message size (DDL_LL_MAX_BYTES, 0 = off)
   size_t ll_slot = 0;
-  char* ll_of(int r) const { return scratch_of(r) + 2 * scratch_half; }
+  char* ll_of(int r) const {
+    if (loopback) return lb_ll + (size_t)r * 2 * (size_t)P * ll_slot;
+    return scratch_of(r) + 2 * scratch_half;
+  }
 };
 
 extern "C" {
@@ -456,8 +460,12 @@ bool plan_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
 // LL one-shot: multi-process only, 8 data bytes per thread and line, the message must fit a
 // receive slot (16 bytes per 8 data bytes); not with DDL_CHECK (no barrier to carry the
 // signature).  ALGO_LL forces it wherever it fits, AUTO up to ll_max bytes.
+// Loopback runs it only when forced (ALGO_LL): all virtual ranks in one cooperative launch,
+// so the kernel can be profiled under kernel serialisation; AUTO keeps LL for the cross-GPU
+// latency regime it is built for.
 bool use_ll(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
-  if (c->loopback || c->P < 2 || c->check) return false;
+  if (c->P < 2 || c->check) return false;
+  if (c->loopback && (c->algo != DDL_ALGO_LL || !c->lb_ll)) return false;
   if (c->algo != DDL_ALGO_LL && c->algo != DDL_ALGO_AUTO) return false;
   const uint64_t bytes = n * (uint64_t)elem_size(dt);
   if (c->algo == DDL_ALGO_AUTO && bytes > c->ll_max) return false;
@@ -1102,6 +1110,7 @@ ddl_result_t ddl_finalize(ddl_comm_t c) {
   if (c->alloc) cudaFree(c->alloc);
   if (c->lb_flags) cudaFree(c->lb_flags);
   if (c->lb_ws) cudaFree(c->lb_ws);
+  if (c->lb_ll) cudaFree(c->lb_ll);
   if (c->err) cudaFree(c->err);
   if (c->trace) cudaFree(c->trace);
   delete c;
@@ -1124,11 +1133,17 @@ ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, in
   }
   cudaError_t e = cudaMalloc(&c->lb_flags, c->flags_bytes * nranks);
   if (e == cudaSuccess) e = cudaMemset(c->lb_flags, 0, c->flags_bytes * nranks);
+  // LL receive regions (forced ALGO_LL only): zeroed, so a stale word never carries a live epoch
+  c->ll_slot = (2 * c->ll_max + 4095) / 4096 * 4096;
+  const size_t ll_bytes = (size_t)nranks * 2 * (size_t)nranks * c->ll_slot;
+  if (e == cudaSuccess && ll_bytes) e = cudaMalloc(&c->lb_ll, ll_bytes);
+  if (e == cudaSuccess && ll_bytes) e = cudaMemset(c->lb_ll, 0, ll_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(int));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (c->lb_flags) cudaFree(c->lb_flags);
+    if (c->lb_ll) cudaFree(c->lb_ll);
     if (c->err) cudaFree(c->err);
     delete c;
     return cuda_fail(e, "ddl_loopback_init allocation");
@@ -1378,6 +1393,15 @@ ddl_result_t ddl_group_allreduce(ddl_comm_t c, void* const* bufs, size_t count, 
   DDL_ON_DEVICE(c->device);
   KParams p = base_params(c, count, op);
   Plan pl;
+  if (use_ll(c, count, dt, &pl)) {
+    for (int m = 0; m < c->P; ++m) {
+      p.cin[m] = bufs[m];
+      p.out[m] = bufs[m];
+      p.ll[m] = c->ll_of(m);
+    }
+    p.ll_slot = c->ll_slot;
+    return launch(c, p, pl, dt, stream);
+  }
   const bool one = use_oneshot(c, count, dt, &pl);
   if (!one) pl = plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true);
   p.q = pl.q;

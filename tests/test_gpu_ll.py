@@ -165,3 +165,31 @@ def test_ll_missing_rank_times_out():
         assert g.async_error() == ddl.ERR_TIMEOUT
     finally:
         g.finalize()
+
+
+@pytest.mark.parametrize("P,dims", CASES + [(8, [4, 1, 2]), (1, [1])],
+                         ids=IDS + ["P8-4.1.2", "P1-1"])
+def test_ll_loopback_parity(P, dims):
+    """The LL kernel in loopback (forced ALGO_LL): all P virtual ranks in one cooperative
+    launch, so it also runs under a serialising profiler; bit-exact vs the oracle, and
+    repeated calls alternate the receive halves (epoch parity) correctly."""
+    lb = ddl.Loopback(P, dims)
+    lb.set_algo(ddl.ALGO_LL, 0)
+    for dtype in ("int32", "float32", "bfloat16"):
+        for op in (["sum"] if dtype == "int32" else ["sum", "avg"]):
+            for n in SIZES[dtype]:
+                if P > 1:
+                    assert lb.algo_for(n, dtype) == ddl.ALGO_LL, (dtype, n)
+                bufs = si.rank_buffers(dtype, KIND[dtype], n, P, seed=n + 5 * P)
+                want = oracle.allreduce(bufs, dims, dtype, op)
+                dev = [to_dev(b, dtype) for b in bufs]
+                lb.all_reduce(dev, op)
+                torch.cuda.synchronize()
+                assert lb.async_error() == ddl.SUCCESS
+                for r in range(P):
+                    got = to_host(dev[r])
+                    assert same_bits(got, want[r]), (dims, dtype, op, n, r, first_diff(got, want[r]))
+    # AUTO in loopback never picks LL (its gain is cross-GPU latency)
+    lb.set_algo(ddl.ALGO_AUTO, 512 << 10)
+    assert lb.algo_for(1000, "float32") != ddl.ALGO_LL
+    lb.finalize()
