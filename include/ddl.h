@@ -89,6 +89,10 @@ typedef enum { DDL_ALGO_AUTO = 0, DDL_ALGO_HIER = 1, DDL_ALGO_ONESHOT = 2, DDL_A
 /* These never touch the GPU; they expose the planner the kernels use, for tests.       */
 
 int ddl_version(void);                                   /* 100 * major + minor           */
+/* Build options: bit 0 = the experiment kernels PATH 3 (DDL_DYN) and PATH 4 (DDL_STEAL)
+ * are compiled in (DDL_EXPERIMENTAL=1 bash build.sh); without them ddl_init /
+ * ddl_loopback_init return DDL_ERR_UNSUPPORTED when DDL_DYN or DDL_STEAL is set. */
+int ddl_build_flags(void);
 const char* ddl_result_string(ddl_result_t r);           /* static string, never NULL     */
 const char* ddl_last_error_string(void);                 /* last CUDA failure text (this thread) */
 

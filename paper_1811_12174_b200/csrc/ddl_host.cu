@@ -20,6 +20,9 @@
 
 using namespace ddl;
 
+#ifndef DDL_EXPERIMENTAL
+#define DDL_EXPERIMENTAL 0  // 1: also compile the PATH 3 / PATH 4 experiment kernels
+#endif
 static_assert(DDL_MAX_RANKS == kMaxRanks, "header / planner rank limit");
 static_assert(DDL_MAX_DIMS == kMaxDims, "header / planner dims limit");
 
@@ -298,6 +301,11 @@ ddl_result_t common_init(ddl_comm* c, int nranks, const int* dims, int ndims, in
                        (size_t)c->cmax * kMaxRanks;             // + DDL_CHECK signatures
   c->flags_bytes = (words * 4 + 65535) / 65536 * 65536;
   apply_env(c);
+#if !DDL_EXPERIMENTAL
+  // the rank-level dynamic (PATH 3) and work-stealing (PATH 4) kernels were measured slower
+  // and are only compiled with DDL_EXPERIMENTAL=1 bash build.sh
+  if (c->use_dyn || c->use_steal) return DDL_ERR_UNSUPPORTED;
+#endif
   preload_kernels();
   if (env_size("DDL_TRACE", 0)) {
     const size_t tb = (size_t)nranks * c->cmax * kTraceEvents * sizeof(uint64_t);
@@ -331,8 +339,12 @@ template <typename T>
 const void* hier_fn(int path) {
   if (path == 6) return (const void*)ddl_hier_kernel<T, 6>;
   if (path == 5) return (const void*)ddl_hier_kernel<T, 5>;
+#if DDL_EXPERIMENTAL
   if (path == 4) return (const void*)ddl_hier_kernel<T, 4>;
   if (path == 3) return (const void*)ddl_dyn_kernel<T>;
+#else
+  if (path == 3 || path == 4) return nullptr;
+#endif
   if (path == 2) return (const void*)ddl_hier_kernel<T, 2>;
   return path == 1 ? (const void*)ddl_hier_kernel<T, 1> : (const void*)ddl_hier_kernel<T, 0>;
 }
@@ -585,7 +597,8 @@ ddl_result_t local_copy(const void* src, void* dst, size_t count, ddl_dtype_t dt
 
 extern "C" {
 
-int ddl_version(void) { return 102; }  // 1.02: grouped all-reduce (ddl_allreduce_many)
+int ddl_version(void) { return 103; }  // 1.03: loopback LL, ddl_peer_buffer, ddl_build_flags
+int ddl_build_flags(void) { return DDL_EXPERIMENTAL ? 1 : 0; }
 
 const char* ddl_result_string(ddl_result_t r) {
   switch (r) {

@@ -52,6 +52,7 @@ def _load() -> ctypes.CDLL:
     pp = ctypes.POINTER(c_void)
     sig = {
         "ddl_version": (c_int, []),
+        "ddl_build_flags": (c_int, []),
         "ddl_result_string": (ctypes.c_char_p, [c_int]),
         "ddl_last_error_string": (ctypes.c_char_p, []),
         "ddl_check_dims": (c_int, [c_int, ip, c_int]),
@@ -101,6 +102,11 @@ def _load() -> ctypes.CDLL:
 
 
 _lib = _load()
+
+
+def has_experimental_kernels() -> bool:
+    """PATH 3 (DDL_DYN) / PATH 4 (DDL_STEAL) compiled in (DDL_EXPERIMENTAL=1 bash build.sh)."""
+    return bool(_lib.ddl_build_flags() & 1)
 
 
 def lib() -> ctypes.CDLL:

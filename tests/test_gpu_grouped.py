@@ -180,6 +180,8 @@ def test_grouped_honours_kernel_variant(env):
     the experimental variants hold for all_reduce_many too: every bucket goes through a
     single call of the selected kernel (the grouped kernel is TMA-only), on the
     loopback and the multi-process launch paths, bit-exact vs the oracle."""
+    if "DDL_STEAL" in env and not ddl.has_experimental_kernels():
+        pytest.skip("PATH 4 not compiled (DDL_EXPERIMENTAL=1 bash build.sh)")
     P, dims = 8, [4, 2]
     lb = with_env(env, lambda: ddl.Loopback(P, dims))
     hosts, devs = make(P, "float32", SIZES, seed=500)

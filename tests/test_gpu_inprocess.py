@@ -71,6 +71,8 @@ IDS = [f"P{P}-{'x'.join(map(str, d))}" for P, d in CASES]
 def test_allreduce_zero_copy_and_staged(P, dims, algo, variant):
     if algo == ddl.ALGO_ONESHOT and variant != "default":
         pytest.skip("variants only change the hierarchical kernel")
+    if variant == "steal" and not ddl.has_experimental_kernels():
+        pytest.skip("PATH 4 not compiled (DDL_EXPERIMENTAL=1 bash build.sh)")
     g = group(P, dims, VARIANTS[variant])
     g.set_algo(algo, 1 << 40 if algo == ddl.ALGO_ONESHOT else 0)
     for dtype in ("int32", "float32", "bfloat16"):
@@ -97,6 +99,8 @@ def test_allreduce_zero_copy_and_staged(P, dims, algo, variant):
 @pytest.mark.parametrize("P,dims", CASES, ids=IDS)
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
 def test_reduce_scatter_allgather_staged(P, dims, variant):
+    if variant == "steal" and not ddl.has_experimental_kernels():
+        pytest.skip("PATH 4 not compiled (DDL_EXPERIMENTAL=1 bash build.sh)")
     g = group(P, dims, VARIANTS[variant])
     for recv in (96, 1001, 50_000):
         for dtype in ("int32", "float32", "bfloat16"):

@@ -273,6 +273,9 @@ PATH_ENVS = {"steal": {"DDL_STEAL": "1"}, "dyn": {"DDL_DYN": "1"}, "ldg": {"DDL_
              "waves-tma-all": {"DDL_WAVES": "5", "DDL_MIN_WAVE_SLICE_BYTES": "0", "DDL_TMA_MIN_SLICE_BYTES": "0"}}
 
 
+EXPERIMENTAL_PATHS = ("steal", "dyn")
+
+
 @pytest.mark.parametrize("path", sorted(PATH_ENVS))
 @pytest.mark.parametrize("P,dims", [(8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (6, [3, 2]), (4, [2, 2])])
 def test_kernel_paths_parity(path, P, dims):
@@ -280,6 +283,8 @@ def test_kernel_paths_parity(path, P, dims):
     stealing, rank-level dynamic, streaming, waves) computes the same bits as the oracle."""
     import os
     envs = PATH_ENVS[path]
+    if path in EXPERIMENTAL_PATHS and not ddl.has_experimental_kernels():
+        pytest.skip("PATH 3/4 experiment kernels not compiled (DDL_EXPERIMENTAL=1 bash build.sh)")
     old = {k: os.environ.get(k) for k in envs}
     os.environ.update(envs)
     try:
@@ -361,3 +366,19 @@ def test_cuda_graph_capture_replay(algo):
         for r in range(P):
             assert same_bits(to_host(bufs[r]), want[r]), (it, r)
     lb.finalize()
+
+
+def test_experiment_kernels_refused_when_not_built():
+    """Without DDL_EXPERIMENTAL=1 at build time, asking for PATH 3 / PATH 4 fails loudly at
+    init (DDL_ERR_UNSUPPORTED) instead of silently running another kernel."""
+    import os
+    if ddl.has_experimental_kernels():
+        pytest.skip("experiment kernels are compiled in")
+    for k in ("DDL_STEAL", "DDL_DYN"):
+        os.environ[k] = "1"
+        try:
+            with pytest.raises(ddl.DDLError) as ei:
+                ddl.Loopback(4, [2, 2])
+            assert ei.value.code == ddl.ERR_UNSUPPORTED
+        finally:
+            os.environ.pop(k, None)
