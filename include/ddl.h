@@ -136,6 +136,34 @@ ddl_result_t ddl_connect(ddl_comm_t comm, const void* all_handles /* nranks * ha
 /* The symmetric zero-copy buffer (max_bytes, 256-B aligned).  An all-reduce on a buffer
  * inside it, at the SAME offset on every rank, reads peers' data in place (no staging). */
 ddl_result_t ddl_buffer(ddl_comm_t comm, void** dev_ptr, size_t* bytes);
+/* NVLS phases (P:L54 (3) "mix and match" per decomposed piece): an
+ * NVSwitch multicast object per live dim's group, so that phase d runs IN the switch --
+ * multimem.ld_reduce for the reduce-scatter (the switch sums the g_d members' copies),
+ * multimem.st for the all-gather (one store reaches every member).  Per GPU that moves
+ * ~S(1+1/P) bytes per direction instead of 2S(P-1)/P.  Setup is collective, in four
+ * rounds; after each of the first three the caller all-gathers every rank's blob
+ * (ddl_nvls_blob_size() bytes, rank order) and passes the result to the next call:
+ *   ddl_nvls_prepare(comm, bytes, mine)      -> all-gather -> all
+ *   ddl_nvls_attach(comm, all, mine)         -> all-gather -> all
+ *   ddl_nvls_bind(comm, all, mine)           -> all-gather -> all
+ *   ddl_nvls_commit(comm, all)               -> DDL_SUCCESS: NVLS on; DDL_ERR_UNSUPPORTED: off
+ * A rank that cannot take part (no multicast support or fabric, one GPU per process not
+ * given, a failed import / bind) reports it in its blob, and commit then turns NVLS off on
+ * every rank (resources released; all calls keep the direct P2P phases) -- never a hang.
+ * Requires ddl_connect first.  `bytes` is the NVLS buffer size per rank (rounded up to the
+ * multicast granularity).  All-reduces of buffers inside ddl_nvls_buffer() (same offset on
+ * every rank, count * size a multiple of 16 B) run the dims in *dims_mask in the switch
+ * (DDL_NVLS_DIMS=bitmask of dims restricts them; default every live dim) and the rest as
+ * direct phases over the peers' unicast mappings.  Numerics: the switch's fold order is not
+ * specified, so fp32 / bf16 results of NVLS phases are gated by the Higham bound instead of
+ * bit-exactness (int32: exact); reading 15. */
+size_t ddl_nvls_blob_size(void);
+ddl_result_t ddl_nvls_prepare(ddl_comm_t comm, size_t bytes, void* blob_out);
+ddl_result_t ddl_nvls_attach(ddl_comm_t comm, const void* all_blobs, void* blob_out);
+ddl_result_t ddl_nvls_bind(ddl_comm_t comm, const void* all_blobs, void* blob_out);
+ddl_result_t ddl_nvls_commit(ddl_comm_t comm, const void* all_blobs);
+ddl_result_t ddl_nvls_buffer(ddl_comm_t comm, void** dev_ptr, size_t* bytes, int* dims_mask);
+
 /* Rank `peer`'s symmetric buffer as mapped into this process (cudaIpc over NVLink; this
  * rank's own buffer for peer == rank).  For measurement and diagnostics (bench.py's
  * peer-copy peak); writing into it races with the peer's collectives unless the caller

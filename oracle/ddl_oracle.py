@@ -33,6 +33,10 @@ blocks, no padding (ledger 4); avg = one multiply by fl32(1/P) of the fully redu
 value, fused into the last RS phase whose g_d > 1 (ledger 5); int32 avg rejected (ledger 6);
 bf16 accumulates in fp32 within a phase and is rounded RNE to bf16 at every phase boundary
 (ledger 7); IEEE RNE everywhere, no FMA, no flush-to-zero (ledger 9); int32 wraps (ledger 11).
+NVLS phases (SURVEY.md 8(f) NEXT-1, P:L54 (3) "mix and match" per piece; DESIGN.md reading
+15): ``allreduce(..., nvls_dims=...)`` runs those dims' RS phases "in the switch" -- one
+admissible result of an unspecified fold order (_switch_sum) -- and ``fold_error_bound``
+gives the bound every fold order meets, which is how NVLS results are gated (int32 exact).
 
 Arithmetic: numpy int32 (wrapping) and float32 (IEEE binary32, round-to-nearest-even, no
 FTZ) elementwise adds, one per step in the order above.  bf16 rounding is written out on
@@ -198,8 +202,26 @@ def _check_buffers(bufs, dtype: str) -> tuple[int, int]:
     return len(bufs), n
 
 
-def _rs_phases(B, dims, dtype, op, n, q, traffic):
-    """one lockstep pass per RS phase, innermost dim first."""
+def _switch_sum(vals, dtype):
+    """An NVLS phase: the NVSwitch returns the group's sum in an order
+    it does not specify (ledger 14: every order is "correct").  The oracle takes one admissible
+    result: the binary64 sum of the members' values, rounded once to binary32 (int32: the
+    exact sum mod 2^32, which every order reaches).  GPU results of NVLS phases are compared
+    with fold_error_bound, never bit for bit (fp32 / bf16)."""
+    if dtype == INT32:
+        acc = vals[0].astype(np.int64)
+        for v in vals[1:]:
+            acc = acc + v.astype(np.int64)
+        return (acc & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+    acc = vals[0].astype(np.float64)
+    for v in vals[1:]:
+        acc = acc + v.astype(np.float64)
+    return acc.astype(np.float32)
+
+
+def _rs_phases(B, dims, dtype, op, n, q, traffic, nvls_dims=()):
+    """one lockstep pass per RS phase, innermost dim first.  Dims in
+    nvls_dims reduce "in the switch" (_switch_sum) instead of the ascending direct fold."""
     P = len(B)
     w = ITEMSIZE[dtype]
     live = [d for d, g in enumerate(dims) if g > 1]
@@ -212,9 +234,12 @@ def _rs_phases(B, dims, dtype, op, n, q, traffic):
                 lo, hi = block_range(b, n, q)
                 if lo == hi:
                     continue
-                acc = _to_acc(snap[members[0]][lo:hi], dtype)
-                for v in range(1, len(members)):
-                    acc = acc + _to_acc(snap[members[v]][lo:hi], dtype)
+                if d in nvls_dims:
+                    acc = _switch_sum([_to_acc(snap[m][lo:hi], dtype) for m in members], dtype)
+                else:
+                    acc = _to_acc(snap[members[0]][lo:hi], dtype)
+                    for v in range(1, len(members)):
+                        acc = acc + _to_acc(snap[members[v]][lo:hi], dtype)
                 if op == "avg" and d == last:
                     acc = acc * avg_scale(P)
                 B[r][lo:hi] = _from_acc(acc, dtype)
@@ -246,9 +271,11 @@ def _ag_phases(B, dims, dtype, n, q, traffic):
 
 
 def allreduce(bufs, dims, dtype: str, op: str = "sum", q: int | None = None,
-              traffic: Traffic | None = None) -> list[np.ndarray]:
+              traffic: Traffic | None = None, nvls_dims=()) -> list[np.ndarray]:
     """ddl_allreduce semantics: returns every rank's buffer after the full schedule
-    RS(d=0..k-1) then AG(d=k-1..0).  Inputs are not modified."""
+    RS(d=0..k-1) then AG(d=k-1..0).  Inputs are not modified.  nvls_dims: the dims whose
+    phases run in the NVSwitch (per-phase algorithm, P:L54 (3)); their RS fold order is the
+    switch's (_switch_sum), their AG is the same bit copy."""
     P, n = _check_buffers(bufs, dtype)
     dims = validate_dims(dims, P)
     if op not in ("sum", "avg"):
@@ -257,7 +284,7 @@ def allreduce(bufs, dims, dtype: str, op: str = "sum", q: int | None = None,
         raise Unsupported("int32 avg is undefined (ledger 6)")
     q = block_elems(n, P, dtype) if q is None else q
     B = [np.array(x, dtype=STORAGE[dtype], copy=True) for x in bufs]
-    _rs_phases(B, dims, dtype, op, n, q, traffic)
+    _rs_phases(B, dims, dtype, op, n, q, traffic, tuple(nvls_dims))
     _ag_phases(B, dims, dtype, n, q, traffic)
     return B
 
@@ -342,3 +369,27 @@ def exact_sum_f64(bufs, dtype: str) -> tuple[np.ndarray, np.ndarray]:
         s += x.astype(np.float64)
         a += np.abs(x.astype(np.float64))
     return s, a
+
+
+def fold_error_bound(bufs, dims, dtype: str, op: str = "sum"):
+    """(s, bound): the exact (binary64) result s -- the sum, or the sum / P for avg -- and a
+    per-element bound on |y - s| that holds for ANY summation order inside the phases (the
+    direct ascending folds and the switch's unspecified NVLS folds alike; ledger 8/14).
+    fp32: every order is a binary tree of P-1 rounded adds, |err| <= gamma_{P-1} sum|x|
+    (Higham 2002, eq. 4.4) with u = 2^-24, plus the avg multiply by fl32(1/P) (2u |s|/P).
+    bf16: additionally one RNE to bf16 (u = 2^-8) at each of the k phase boundaries.  A tiny
+    absolute term covers subnormal results (no flush: ledger 9)."""
+    P = len(bufs)
+    s64, a64 = exact_sum_f64(bufs, dtype)
+    k = sum(1 for g in dims if g > 1)
+    u = 2.0 ** -24
+    g = (P - 1) * u / (1 - (P - 1) * u)
+    if dtype == BFLOAT16:
+        ub = 2.0 ** -8
+        bound = (k * ub + g * (1 + ub) ** k) * (1 + ub) ** k * a64
+    else:
+        bound = g * a64
+    tiny = P * 2.0 ** -149
+    if op == "avg":
+        return s64 / P, bound / P + 3 * u * np.abs(s64) / P + tiny
+    return s64, bound + tiny

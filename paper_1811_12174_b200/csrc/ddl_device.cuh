@@ -73,7 +73,9 @@ struct KParams {
                        // evict_first (final, never re-read in the call); bit 2: later RS phases'
                        // loads evict_first (partials, consumed); bit 3: non-last RS phases' stores
                        // evict_last (partials the next phase reads); bit 4: also the last RS
-                       // phase's stores (off: they would linger as evict_last after the call)
+                       // phase's stores (off: they would linger as evict_last after the call);
+                       // bit 5: bit 1 only for the last AG phase (earlier AG phases' stores are
+                       // the next AG phase's sources); bit 6: those earlier stores evict_last
   int nwaves;          // hier: slices per CTA, run one after another (wave w = slice w*gridDim.x + blockIdx.x)
   uint64_t* trace;     // debug (DDL_TRACE=1): [P][cmax][kTraceEvents] globaltimer stamps, else null
   int stream_every;    // PATH 5: publish progress every k chunks (and at the phase end)
@@ -82,8 +84,17 @@ struct KParams {
   uint64_t scratch_half;     // bytes per half
   char* ll[kMaxRanks];       // LL one-shot: each rank's receive region (two halves of P slots)
   uint64_t ll_slot;          // bytes per source slot (half = P slots)
+  // NVLS phases (PATH 7): mc[d] = this rank's dim-d group multicast
+  // mapping at the buffer's offset; dims whose bit is set in nvls_mask reduce with
+  // multimem.ld_reduce (RS) and broadcast with multimem.st (AG), the others run the
+  // register-staged direct phases over the peers' unicast mappings
+  char* mc[kMaxDims];
+  int nvls_mask;
+  int nvls_emulate;  // test hook (DDL_NVLS_EMULATE=1): the NVLS phases' data flow done with unicast
+                     // loads / stores (RS folds the members in DESCENDING coordinate -- an order
+                     // other than the direct path's; AG stores each own vector into every member)
 };
-constexpr int kTraceEvents = 40;
+constexpr int kTraceEvents = 128;
 
 // This CTA's index within its rank and the rank's CTA count (the grid is (ctas, P) in
 // loopback, or transposed to (P, ctas) for the grouped kernel with DDL_TRANSPOSE=1).
@@ -795,7 +806,13 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
     } else if (threadIdx.x == 0) {
       // copy: one bulk store from the stage (async proxy); the stage is reusable once the
       // store has read it
-      if (x.kind == kPhAG && (p.l2hint & 2)) tma_store_hint(pd, sbase, bytes, policy_evict_first());
+      // AG stores: evict_first (bit 1) -- with bit 5 only in the LAST allgather phase, whose
+      // stores nobody reads again in the call; an earlier AG phase's stores are the next AG
+      // phase's sources (normal priority, or evict_last with bit 6)
+      const bool ag_first = x.kind == kPhAG && (p.l2hint & 2) && (x.last || !(p.l2hint & 32));
+      const bool ag_last = x.kind == kPhAG && !x.last && (p.l2hint & 64);
+      if (ag_first) tma_store_hint(pd, sbase, bytes, policy_evict_first());
+      else if (ag_last) tma_store_hint(pd, sbase, bytes, policy_evict_last());
       else tma_store(pd, sbase, bytes);
       tma_store_wait_read();
     }
@@ -813,17 +830,119 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
 
 // Experimental kernel variants (PATH 3 rank-level dynamic, PATH 4 work stealing, PATH 5
 // streaming): parity-tested, measured slower than PATH 2 in loopback.
+// ------------------------------------------------------------------------ NVLS phases (PATH 7)
+// "mix and match ... reduce-scatter and all-gather implementations" per decomposed piece
+// (P:L54 (3)): on an NVSwitch with multicast (NVLS), phase d of a group can run IN the switch.
+// RS: rank r loads each 16-B vector of its blocks A_{d+1}(r) through the group's multicast
+// address with multimem.ld_reduce -- the switch returns the sum over the g_d members' copies
+// (fold order chosen by the switch: not the direct path's ascending order, so fp32 / bf16
+// are tolerance-gated, int32 stays exact) -- applies the fused 1/P scale in the last RS
+// phase and stores locally.  AG: rank r multicast-stores its blocks A_{d+1}(r) once
+// (multimem.st): the switch writes them into every member.  Per GPU that moves ~S(1+1/P)
+// bytes per direction instead of 2S(P-1)/P.  Buffers are 16-B multiples (host-checked), so
+// spans have no ragged tail.  Accesses through the multicast alias and the unicast alias of
+// the same memory are ordered with fence.proxy.alias around every phase (and the device
+// barriers' release/acquire at .sys scope order them across GPUs).
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
+template <typename T>
+__device__ __forceinline__ uint4 mc_ld_reduce(const char* a);
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<float>(const char* a) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<__nv_bfloat16>(const char* a) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<int32_t>(const char* a) {
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.s32 %0, [%1];" : "=r"(w[k]) : "l"(a + 4 * k) : "memory");
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ void mc_st(char* a, const uint4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(a), "f"(__uint_as_float(v.x)),
+               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+               : "memory");
+}
+
+template <typename T>
+__device__ void nvls_phase(const KParams& p, int me, const PhaseCtx& x) {
+  using A = typename Tr<T>::Acc;
+  constexpr int W = Tr<T>::W;
+  const Topo& t = p.t;
+  const int nb = nblocks(t, x.d + 1);
+  const bool rs = x.kind == kPhRS;
+  const bool do_scale = rs && x.last && p.op == kAvg;
+  char* mc = p.mc[x.d];
+  char* dst = dst_base(p, me, x);
+  const char* own = static_cast<const char*>(p.work[me]);
+  fence_proxy_alias();
+  for (int u = 0; u < nb; ++u) {
+    const Span sp = slice_span<W>(p, block_of(t, me, x.d + 1, u), x.s);  // RS: reduce; AG: broadcast
+    for (uint32_t i = threadIdx.x; i < sp.nvec; i += blockDim.x) {
+      const size_t off = (sp.e0 + (uint64_t)i * W) * sizeof(T);
+      if (p.nvls_emulate) {
+        if (rs) {
+          A a[W];
+          for (int v = x.g - 1; v >= 0; --v) {
+            const int m = member(t, me, x.d, v);
+            A y[W];
+            unpack<T>(ld_vec(static_cast<const char*>(x.first ? p.in[m] : p.work[m]) + off), y);
+#pragma unroll
+            for (int k = 0; k < W; ++k) a[k] = v == x.g - 1 ? y[k] : Tr<T>::add(a[k], y[k]);
+          }
+          if (do_scale) {
+#pragma unroll
+            for (int k = 0; k < W; ++k) a[k] = Tr<T>::mul(a[k], p.scale);
+          }
+          st_vec(dst + off, pack<T>(a));
+        } else {
+          const uint4 v = ld_vec(own + off);
+          for (int l = 0; l < t.g[x.d]; ++l) st_vec(static_cast<char*>(p.work[member(t, me, x.d, l)]) + off, v);
+        }
+        continue;
+      }
+      if (rs) {
+        uint4 v = mc_ld_reduce<T>(mc + off);
+        if (do_scale) {
+          A a[W];
+          unpack<T>(v, a);
+#pragma unroll
+          for (int k = 0; k < W; ++k) a[k] = Tr<T>::mul(a[k], p.scale);
+          v = pack<T>(a);
+        }
+        st_vec(dst + off, v);
+      } else {
+        mc_st(mc + off, ld_vec(own + off));
+      }
+    }
+  }
+  fence_proxy_alias();
+}
+
 #include "ddl_device_variants.cuh"
 
 // ------------------------------------------------------------------------ the hierarchical kernel
 // PATH: 0 = element-wise loads (unaligned RS/AG layouts), 1 = 16-byte register-staged
 // loads, 2 = 16-byte TMA-staged (default), 4 = TMA-staged with work stealing, 5 = streaming,
-// 6 = TMA-staged in waves (large messages).
+// 6 = TMA-staged in waves (large messages), 7 = NVLS phases (multimem) where p.nvls_mask says,
+// register-staged direct phases elsewhere.
 template <typename T, int PATH>
-__global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kThreads, (PATH >= 2 && PATH != 7) ? DDL_TMA_MINBLOCKS : 1) ddl_hier_kernel(const __grid_constant__ KParams p) {
   pdl_begin();
   constexpr bool VEC = PATH >= 1;
-  constexpr bool TMA = PATH >= 2;
+  constexpr bool NVLS = PATH == 7;  // NVLS phases where nvls_mask says, register-staged elsewhere
+  constexpr bool TMA = PATH >= 2 && !NVLS;
   constexpr bool STEAL = PATH == 4;
   constexpr bool STREAM = PATH == 5;
   constexpr bool WAVES = PATH == 6;
@@ -851,6 +970,13 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
         steal_phase<T>(p, me, x, pp, j);
         return;
       }
+    }
+    if constexpr (NVLS) {
+      if ((x.kind == kPhRS || x.kind == kPhAG) && ((p.nvls_mask >> x.d) & 1)) {
+        nvls_phase<T>(p, me, x);
+        return;
+      }
+      fence_proxy_alias();  // sources may have been written through a multicast alias
     }
     if constexpr (TMA) tma_phase<T>(p, me, x, pp);
     else ldg_phase<T, VEC>(p, me, x);
@@ -920,8 +1046,21 @@ __global__ void __launch_bounds__(kThreads, PATH >= 2 ? DDL_TMA_MINBLOCKS : 1) d
         if (!(STREAM && (p.mode & kRS)) && !((p.mode & kRS) == 0 && jj == 0 && w > 0 && !cin) &&
             !dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j), jj == 0 && !(p.mode & kRS) && w == 0))
           return;
+        if constexpr (NVLS) {
+          // an NVLS allgather PUSHES (multimem.st) into the members of its group: before this
+          // rank forwards what it received, the previous AG phase's group must have finished
+          // pushing into it -- a barrier with that group too (its own slot, 2L+jj)
+          const int pd = jj > 0 ? t.live[L - jj] : -1;
+          if (pd >= 0 && ((p.nvls_mask >> pd) & 1)) {
+            auto pushers = [&t, me_, pd](int l) {
+              const int c = coord(t, me_, pd);
+              return member(t, me_, pd, l < c ? l : l + 1);
+            };
+            if (!dbarrier(p, me, 2 * L + jj, t.g[pd] - 1, ew, pushers)) return;
+          }
+        }
         if (tr) trace_ev(p, me, 2 + 2 * j);
-        prev = ctx(kPhAG, t.live[L - 1 - jj], false, false);
+        prev = ctx(kPhAG, t.live[L - 1 - jj], false, jj == L - 1);
         run(prev, j);
         have_prev = true;
         if (tr) trace_ev(p, me, 3 + 2 * j);
@@ -1035,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
       const int j = L + jj;
       if (!dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j))) return;
       tev(k, j, 0);
-      PhaseCtx x = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, false);
+      PhaseCtx x = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, jj == L - 1);
       x.s = w * cc + lc;
       tma_phase<T>(p, me, x, pp);
       tev(k, j, 1);

@@ -17,6 +17,7 @@
 #include "ddl.h"
 #include "ddl_device.cuh"
 #include "ddl_plan.h"
+#include "ddl_nvls.h"
 
 using namespace ddl;
 
@@ -154,6 +155,8 @@ struct ddl_comm {
   int transpose = 1;                       // DDL_TRANSPOSE: loopback grids (P, ctas) (profiles/r01_transpose_ab.txt)
   int l2hint = 15;                         // DDL_L2_HINTS: KParams::l2hint bits (profiles/r01_l2_hints.txt)
   int group_waves = 1;                     // DDL_GROUP_WAVES: waves per bucket in a grouped all-reduce (0 = auto)
+  size_t group_wave_bytes = 0;             // DDL_GROUP_WAVE_MB: per-wave partial footprint budget (0 = off)
+  int group_order = 0;                     // DDL_GROUP_ORDER: 0 LPT (longest first), 1 ascending within a channel
   int waves = 0;                           // DDL_WAVES: slices per CTA per hierarchical call (0 = auto)
   size_t wave_slice_bytes = 112 << 10;     // auto: target per-CTA slice of one wave
   size_t min_wave_slice_bytes = 16 << 10;  // no waves below this slice size
@@ -191,6 +194,10 @@ struct ddl_comm {
   // LL receive region after the scratch: two halves of P slots of ll_slot bytes
   size_t ll_max = 64 << 10;  // AUTO uses LL up to this message size (DDL_LL_MAX_BYTES, 0 = off)
   size_t ll_slot = 0;
+  nvls::State nvls;          // NVLS phases (ddl_nvls_*), multi-process only
+  int nvls_dims_mask = -1;   // DDL_NVLS_DIMS: which live dims may run in the switch (bit d; -1 all)
+  bool nvls_emulate = false; // DDL_NVLS_EMULATE=1 (test hook): hierarchical calls run PATH 7 with the
+                             // NVLS phases' data flow emulated by unicast accesses (one GPU)
   char* ll_of(int r) const {
     if (loopback) return lb_ll + (size_t)r * 2 * (size_t)P * ll_slot;
     return scratch_of(r) + 2 * scratch_half;
@@ -263,6 +270,10 @@ void apply_env(ddl_comm* c) {
   c->use_pdl = env_size("DDL_PDL", 1) != 0;
   c->channels = (int)env_size("DDL_CHANNELS", c->channels);
   c->group_waves = (int)env_size("DDL_GROUP_WAVES", c->group_waves);
+  c->group_wave_bytes = env_size("DDL_GROUP_WAVE_MB", c->group_wave_bytes >> 20) << 20;
+  c->group_order = (int)env_size("DDL_GROUP_ORDER", c->group_order);
+  c->nvls_dims_mask = std::getenv("DDL_NVLS_DIMS") ? (int)env_size("DDL_NVLS_DIMS", 0) : -1;
+  c->nvls_emulate = env_size("DDL_NVLS_EMULATE", 0) != 0;
   c->l2hint = (int)env_size("DDL_L2_HINTS", c->l2hint);
   c->transpose = (int)env_size("DDL_TRANSPOSE", c->transpose);
   if (c->channels < 1) c->channels = 1;
@@ -337,6 +348,7 @@ struct Plan {
 
 template <typename T>
 const void* hier_fn(int path) {
+  if (path == 7) return (const void*)ddl_hier_kernel<T, 7>;
   if (path == 6) return (const void*)ddl_hier_kernel<T, 6>;
   if (path == 5) return (const void*)ddl_hier_kernel<T, 5>;
 #if DDL_EXPERIMENTAL
@@ -382,7 +394,7 @@ const void* hier_fn_dt(ddl_dtype_t dt, int path) {
   if (dt == DDL_FLOAT32) return hier_fn<float>(path);
   return hier_fn<__nv_bfloat16>(path);
 }
-size_t hier_smem(int path) { return path >= 2 ? kTmaSmem : 0; }
+size_t hier_smem(int path) { return (path >= 2 && path != 7) ? kTmaSmem : 0; }
 const void* oneshot_fn_dt(ddl_dtype_t dt, int K, int R) {
   if (dt == DDL_INT32) return oneshot_fn<int32_t>(K, R);
   if (dt == DDL_FLOAT32) return oneshot_fn<float>(K, R);
@@ -539,6 +551,26 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
                                 : hier_fn_dt(dt, pl.path);
   if (!fn) return DDL_ERR_UNSUPPORTED;
   if (!pl.oneshot && !pl.ll && pl.slice * (uint64_t)elem_size(dt) > kMaxSliceBytes) return DDL_ERR_TOO_LARGE;
+  if (c->nvls_emulate && !pl.oneshot && !pl.ll && pl.vec && pl.path != 7 && (p.mode & (kRS | kAG)) &&
+      (p.n * (uint64_t)elem_size(dt)) % 16 == 0) {
+    // test hook: the same call through PATH 7 with every live dim's phases "in the switch",
+    // emulated by unicast accesses (so the NVLS data flow runs on one GPU)
+    Plan pe = pl;
+    pe.path = 7;
+    pe.nwaves = 1;
+    const int cap = cap_per_rank(c, hier_fn_dt(dt, 7), 0);
+    if (pe.nctas > cap) {
+      const uint64_t W = 16 / elem_size(dt);
+      uint64_t slice = (pe.q + cap - 1) / cap;
+      slice = (slice + W - 1) / W * W;
+      pe.slice = slice;
+      pe.nctas = (int)((pe.q + slice - 1) / slice);
+      p.slice = slice;
+    }
+    p.nvls_emulate = 1;
+    p.nvls_mask = c->nvls_dims_mask & ((1 << kMaxDims) - 1);
+    return launch(c, p, pe, dt, stream);
+  }
   p.nwaves = (pl.oneshot || pl.ll) ? 1 : pl.nwaves;
   const size_t smem = (pl.oneshot || pl.ll) ? 0 : hier_smem(pl.path);
   blocks_per_sm(fn, smem);  // sets the dynamic shared-memory attribute once
@@ -557,6 +589,59 @@ ddl_result_t launch(const ddl_comm* c, const KParams& p0, const Plan& pl, ddl_dt
     DDL_CUDA(launch_ex(fn, dim3(pl.nctas), smem, s, args, false, c->use_pdl));
   }
   return DDL_SUCCESS;
+}
+
+// ---------------------------------------------------------------- NVLS (ddl_nvls.h)
+bool nvls_owns(const ddl_comm* c, const void* buf, size_t bytes) {
+  const char* b = static_cast<const char*>(buf);
+  return c->nvls.stage == 4 && c->nvls.uc[c->rank] && b >= c->nvls.uc[c->rank] &&
+         b + bytes <= c->nvls.uc[c->rank] + c->nvls.bytes;
+}
+
+// An all-reduce of a buffer inside the NVLS region: the hierarchical schedule with the
+// switch running the phases of the dims in nvls.mask (PATH 7), zero-copy through every
+// rank's unicast mapping of its NVLS memory; the one-shot / LL regimes and counts that are
+// not whole 16-B vectors keep the direct kernels on the same mappings.
+ddl_result_t nvls_allreduce(const ddl_comm* c, KParams& p, void* buf, size_t count, ddl_dtype_t dt, void* stream) {
+  const size_t off = (size_t)(static_cast<char*>(buf) - c->nvls.uc[c->rank]);
+  const int w = elem_size(dt);
+  Plan pl;
+  const bool one = use_oneshot(c, count, dt, &pl);
+  const bool vec = (count * (size_t)w) % 16 == 0;
+  if (!one) {
+    pl = plan_hier(c, count, block_elems(count, c->P, w), dt, true);
+    if (vec && c->nvls.mask) {  // PATH 7: register-staged kernel with the NVLS phases compiled in
+      pl.path = 7;
+      pl.nwaves = 1;
+      const int cap = cap_per_rank(c, hier_fn_dt(dt, 7), 0);
+      if (pl.nctas > cap) {
+        uint64_t slice = (pl.q + cap - 1) / cap;
+        slice = (slice + 16 / w - 1) / (16 / w) * (16 / w);
+        pl.slice = slice;
+        pl.nctas = (int)((pl.q + slice - 1) / slice);
+      }
+      for (int d = 0; d < c->topo.k; ++d) p.mc[d] = c->nvls.mcva[d] ? c->nvls.mcva[d] + off : nullptr;
+      p.nvls_mask = c->nvls.mask;
+    }
+  }
+  p.q = pl.q;
+  p.slice = pl.slice;
+  for (int m = 0; m < c->P; ++m) {
+    char* base = c->nvls.uc[m] + off;
+    p.in[m] = base;
+    p.work[m] = base;
+    p.out[m] = base;
+  }
+  if (one) {  // inputs published through the scratch halves, as for any one-shot call
+    p.mode = kScratch;
+    p.cin[c->rank] = buf;
+    p.out[c->rank] = buf;
+    for (int m = 0; m < c->P; ++m) p.scratch[m] = c->scratch_of(m);
+    p.scratch_half = c->scratch_half;
+  } else {
+    p.mode = kRS | kAG;
+  }
+  return launch(c, p, pl, dt, stream);
 }
 
 ddl_result_t check_common(const ddl_comm* c, ddl_dtype_t dt, ddl_op_t op) {
@@ -786,6 +871,198 @@ ddl_result_t ddl_connect(ddl_comm_t c, const void* all_handles) {
   return DDL_SUCCESS;
 }
 
+// ------------------------------------------------------------------ NVLS setup rounds
+size_t ddl_nvls_blob_size(void) { return sizeof(nvls::Blob); }
+
+static nvls::Blob* blob_of(const void* all, int r) {
+  return reinterpret_cast<nvls::Blob*>(const_cast<char*>(static_cast<const char*>(all)) + (size_t)r * sizeof(nvls::Blob));
+}
+static void blob_init(ddl_comm* c, nvls::Blob* b) {
+  std::memset(b, 0, sizeof(*b));
+  b->magic = nvls::kBlobMagic;
+  b->rank = c->rank;
+  b->pid = (int32_t)getpid();
+  b->phys_fd = -1;
+  for (int d = 0; d < kMaxDims; ++d) b->mc_fd[d] = -1;
+}
+// every rank's blob of this round is well-formed and OK
+static bool all_ok(const ddl_comm* c, const void* all) {
+  for (int r = 0; r < c->P; ++r) {
+    const nvls::Blob* b = blob_of(all, r);
+    if (b->magic != nvls::kBlobMagic || b->rank != r || b->status != nvls::kOk) return false;
+  }
+  return true;
+}
+
+ddl_result_t ddl_nvls_prepare(ddl_comm_t c, size_t bytes, void* out) {
+  if (!c || !out || c->loopback || !c->connected || bytes == 0) return DDL_ERR_INVALID_ARGUMENT;
+  DDL_ON_DEVICE(c->device);
+  nvls::Blob* b = static_cast<nvls::Blob*>(out);
+  blob_init(c, b);
+  nvls::teardown(c->nvls, c->topo, c->rank);
+  nvls::State& s = c->nvls;
+  s.dev = c->device;
+  nvls::Api& a = nvls::api();
+  if (!a.ok || c->P < 2) { b->status = nvls::kNoApi; return DDL_SUCCESS; }
+  int mcs = 0;
+  if (a.getAttr(&mcs, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, c->device) != CUDA_SUCCESS || !mcs) {
+    b->status = nvls::kNoMulticast;
+    return DDL_SUCCESS;
+  }
+  // granularity: the multicast granularity for the largest group, and the allocation one
+  size_t gran = 2u << 20;
+  for (int li = 0; li < c->topo.nlive; ++li) {
+    CUmulticastObjectProp mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.numDevices = (unsigned)c->topo.g[c->topo.live[li]];
+    mp.size = bytes;
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    size_t g = 0;
+    // the minimum granularity (2 MiB here): the recommended one is 512 MiB per rank
+    if (a.mcGranularity(&g, &mp, CU_MULTICAST_GRANULARITY_MINIMUM) == CUDA_SUCCESS && g > gran) gran = g;
+  }
+  s.bytes = (bytes + gran - 1) / gran * gran;
+  b->bytes = s.bytes;
+  // this rank's NVLS memory: exportable by fabric handle if possible, else by file descriptor
+  for (CUmemAllocationHandleType ht : {CU_MEM_HANDLE_TYPE_FABRIC, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR}) {
+    CUmemAllocationProp ap;
+    std::memset(&ap, 0, sizeof(ap));
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = c->device;
+    ap.requestedHandleTypes = ht;
+    if (a.memCreate(&s.phys, s.bytes, &ap, 0) == CUDA_SUCCESS) {
+      s.htype = ht;
+      break;
+    }
+    s.phys = 0;
+  }
+  if (!s.phys) { b->status = nvls::kAllocFailed; return DDL_SUCCESS; }
+  b->htype = (int32_t)s.htype;
+  if (s.htype == CU_MEM_HANDLE_TYPE_FABRIC) {
+    if (a.memExport(&b->phys_fab, s.phys, s.htype, 0) != CUDA_SUCCESS) { b->status = nvls::kAllocFailed; return DDL_SUCCESS; }
+  } else {
+    int fd = -1;
+    if (a.memExport(&fd, s.phys, s.htype, 0) != CUDA_SUCCESS) { b->status = nvls::kAllocFailed; return DDL_SUCCESS; }
+    s.phys_fd = fd;
+    b->phys_fd = fd;
+  }
+  // the multicast object of every live dim whose group I lead (c_d = 0)
+  for (int li = 0; li < c->topo.nlive; ++li) {
+    const int d = c->topo.live[li];
+    if (coord(c->topo, c->rank, d) != 0) continue;
+    CUmulticastObjectProp mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.numDevices = (unsigned)c->topo.g[d];
+    mp.size = s.bytes;
+    mp.handleTypes = s.htype;
+    if (a.mcCreate(&s.mc[d], &mp) != CUDA_SUCCESS) { s.mc[d] = 0; b->status = nvls::kCreateFailed; return DDL_SUCCESS; }
+    if (s.htype == CU_MEM_HANDLE_TYPE_FABRIC) {
+      if (a.memExport(&b->mc_fab[d], s.mc[d], s.htype, 0) != CUDA_SUCCESS) { b->status = nvls::kCreateFailed; return DDL_SUCCESS; }
+    } else {
+      int fd = -1;
+      if (a.memExport(&fd, s.mc[d], s.htype, 0) != CUDA_SUCCESS) { b->status = nvls::kCreateFailed; return DDL_SUCCESS; }
+      s.mc_fd[d] = fd;
+      b->mc_fd[d] = fd;
+    }
+  }
+  s.stage = 1;
+  b->status = nvls::kOk;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_nvls_attach(ddl_comm_t c, const void* all, void* out) {
+  if (!c || !all || !out || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  DDL_ON_DEVICE(c->device);
+  nvls::Blob* b = static_cast<nvls::Blob*>(out);
+  blob_init(c, b);
+  nvls::State& s = c->nvls;
+  nvls::Api& a = nvls::api();
+  if (s.stage != 1 || !all_ok(c, all)) { b->status = nvls::kPeerFailed; return DDL_SUCCESS; }
+  for (int r = 0; r < c->P; ++r)
+    if (blob_of(all, r)->bytes != s.bytes || blob_of(all, r)->htype != (int32_t)s.htype) {
+      b->status = nvls::kPeerFailed;
+      return DDL_SUCCESS;
+    }
+  // unicast mappings: my memory and every peer's
+  if (nvls::map_rw(s.phys, s.bytes, 0, c->device, &s.uc[c->rank]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
+  for (int m = 0; m < c->P; ++m) {
+    if (m == c->rank) continue;
+    const nvls::Blob* pb = blob_of(all, m);
+    if (nvls::import_handle(&s.peer_phys[m], s.htype, pb->pid, pb->phys_fd, &pb->phys_fab) != CUDA_SUCCESS) {
+      s.peer_phys[m] = 0;
+      b->status = nvls::kImportFailed;
+      return DDL_SUCCESS;
+    }
+    if (nvls::map_rw(s.peer_phys[m], s.bytes, 0, c->device, &s.uc[m]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
+  }
+  // join every live dim's group multicast object
+  for (int li = 0; li < c->topo.nlive; ++li) {
+    const int d = c->topo.live[li];
+    const int lead = member(c->topo, c->rank, d, 0);
+    if (lead != c->rank) {
+      const nvls::Blob* lb = blob_of(all, lead);
+      if (nvls::import_handle(&s.mc[d], s.htype, lb->pid, lb->mc_fd[d], &lb->mc_fab[d]) != CUDA_SUCCESS) {
+        s.mc[d] = 0;
+        b->status = nvls::kImportFailed;
+        return DDL_SUCCESS;
+      }
+    }
+    if (a.mcAddDevice(s.mc[d], c->device) != CUDA_SUCCESS) { b->status = nvls::kAddFailed; return DDL_SUCCESS; }
+    s.mc_added[d] = true;
+  }
+  s.stage = 2;
+  b->status = nvls::kOk;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_nvls_bind(ddl_comm_t c, const void* all, void* out) {
+  if (!c || !all || !out || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  DDL_ON_DEVICE(c->device);
+  nvls::Blob* b = static_cast<nvls::Blob*>(out);
+  blob_init(c, b);
+  nvls::State& s = c->nvls;
+  nvls::Api& a = nvls::api();
+  if (s.stage != 2 || !all_ok(c, all)) { b->status = nvls::kPeerFailed; return DDL_SUCCESS; }
+  for (int li = 0; li < c->topo.nlive; ++li) {  // every member has added its device: bind and map
+    const int d = c->topo.live[li];
+    if (a.mcBindMem(s.mc[d], 0, s.phys, 0, s.bytes, 0) != CUDA_SUCCESS) { b->status = nvls::kBindFailed; return DDL_SUCCESS; }
+    s.mc_bound[d] = true;
+    if (nvls::map_rw(s.mc[d], s.bytes, 0, c->device, &s.mcva[d]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
+  }
+  s.stage = 3;
+  b->status = nvls::kOk;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_nvls_commit(ddl_comm_t c, const void* all) {
+  if (!c || !all || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  DDL_ON_DEVICE(c->device);
+  nvls::State& s = c->nvls;
+  if (s.stage != 3 || !all_ok(c, all)) {
+    nvls::teardown(s, c->topo, c->rank);
+    return DDL_ERR_UNSUPPORTED;
+  }
+  DDL_CUDA(cudaMemset(s.uc[c->rank], 0, s.bytes));
+  DDL_CUDA(cudaDeviceSynchronize());
+  s.mask = 0;
+  for (int li = 0; li < c->topo.nlive; ++li) {
+    const int d = c->topo.live[li];
+    if (c->nvls_dims_mask & (1 << d)) s.mask |= 1 << d;
+  }
+  s.stage = 4;
+  return DDL_SUCCESS;
+}
+
+ddl_result_t ddl_nvls_buffer(ddl_comm_t c, void** dev_ptr, size_t* bytes, int* dims_mask) {
+  if (!c || !dev_ptr || !bytes || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
+  if (c->nvls.stage != 4) return DDL_ERR_UNSUPPORTED;
+  *dev_ptr = c->nvls.uc[c->rank];
+  *bytes = c->nvls.bytes;
+  if (dims_mask) *dims_mask = c->nvls.mask;
+  return DDL_SUCCESS;
+}
+
 ddl_result_t ddl_peer_buffer(ddl_comm_t c, int peer, void** dev_ptr, size_t* bytes) {
   if (!c || !dev_ptr || !bytes || c->loopback || peer < 0 || peer >= c->P) return DDL_ERR_INVALID_ARGUMENT;
   if (peer != c->rank && !c->peer_mapped[peer]) return DDL_ERR_NOT_CONNECTED;
@@ -816,10 +1093,11 @@ ddl_result_t ddl_allreduce(ddl_comm_t c, void* buf, size_t count, ddl_dtype_t dt
     if (g.used && (char*)buf >= g.local && (char*)buf + bytes <= g.local + g.bytes) reg = &g;
   }
   const bool zero_copy = in_sym || reg;
-  if (!zero_copy && bytes > c->max_bytes) return DDL_ERR_TOO_LARGE;
   DDL_ON_DEVICE(c->device);
   KParams p = base_params(c, count, op);
   Plan pl;
+  const bool in_nvls = !zero_copy && nvls_owns(c, buf, bytes);
+  if (!zero_copy && !in_nvls && bytes > c->max_bytes) return DDL_ERR_TOO_LARGE;
   if (use_ll(c, count, dt, &pl)) {
     p.cin[c->rank] = buf;
     p.out[c->rank] = buf;
@@ -827,6 +1105,7 @@ ddl_result_t ddl_allreduce(ddl_comm_t c, void* buf, size_t count, ddl_dtype_t dt
     p.ll_slot = c->ll_slot;
     return launch(c, p, pl, dt, stream);
   }
+  if (in_nvls) return nvls_allreduce(c, p, buf, count, dt, stream);
   const bool one = use_oneshot(c, count, dt, &pl);
   if (!one) pl = plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true);
   p.q = pl.q;
@@ -1118,6 +1397,7 @@ ddl_result_t ddl_finalize(ddl_comm_t c) {
   cudaDeviceSynchronize();
   for (int k = 0; k < ddl_comm::kMaxRegs; ++k)
     if (c->regs[k].used) release_reg(c, k);
+  if (!c->loopback) nvls::teardown(c->nvls, c->topo, c->rank);
   for (int m = 0; m < kMaxRanks; ++m)
     if (c->peer_mapped[m]) cudaIpcCloseMemHandle(c->peer_base[m]);
   if (c->alloc) cudaFree(c->alloc);
@@ -1245,11 +1525,14 @@ static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* co
       if (ch < kMaxChannels) mp.bk0[ch] = pos;
       if (ch < K) {
         int k = 0;
+        const int first = pos;
         for (int i = 0; i < gn; ++i)
           if (chan_of[i] == ch) {
             mp.order[pos++] = i;
             ++k;
           }
+        if (c->group_order == 1)  // ascending size within the channel
+          std::stable_sort(mp.order + first, mp.order + pos, [&](int a, int b) { return ns[g0 + a] < ns[g0 + b]; });
         maxk = std::max(maxk, k);
       }
     }
@@ -1268,6 +1551,13 @@ static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* co
       // other channels stream.
       int gw = c->group_waves;
       if (gw == 0) gw = (int)std::min<uint64_t>(32, (slice * w + c->wave_slice_bytes / 2) / c->wave_slice_bytes);
+      // Footprint budget (every rank on this GPU): the first RS phase leaves P * n * w / g_0
+      // bytes of partials in this GPU's memory for the next phase; cut the bucket into waves
+      // so that one wave's partials fit the budget (they then stay in L2 until consumed).
+      if (c->group_wave_bytes && c->gpu_share == c->P && c->topo.nlive > 1) {
+        const uint64_t fp = (uint64_t)c->P * n * w / (uint64_t)c->topo.g[c->topo.live[0]];
+        gw = std::max<int>(gw, (int)std::min<uint64_t>(32, (fp + c->group_wave_bytes - 1) / c->group_wave_bytes));
+      }
       if (slice * w > kMaxSliceBytes)  // 32-bit slice fields: cut into waves
         gw = std::max<int>(gw, (int)((slice * w + kMaxSliceBytes - 1) / kMaxSliceBytes));
       if (gw > 1) {
@@ -1315,7 +1605,7 @@ static void preload_kernels() {
   std::call_once(once, [] {
     std::vector<const void*> fns;
     for (ddl_dtype_t dt : {DDL_INT32, DDL_FLOAT32, DDL_BFLOAT16}) {
-      for (int path = 0; path <= 6; ++path) fns.push_back(hier_fn_dt(dt, path));
+      for (int path = 0; path <= 7; ++path) fns.push_back(hier_fn_dt(dt, path));
       for (int K = 1; K <= 4; ++K) {
         fns.push_back(ll_fn_dt(dt, K));
         for (int R : {1, 2, 4}) fns.push_back(oneshot_fn_dt(dt, K, R));

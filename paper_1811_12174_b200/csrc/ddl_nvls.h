@@ -1,0 +1,205 @@
+// ddl_nvls.h -- host side of the NVLS phases (§2.1
+// feature (3): "mix and match" reduce-scatter / all-gather implementations per decomposed
+// piece).  Included by ddl_host.cu only.
+//
+// An NVSwitch multicast object per (live dim d, group): the group's leader (c_d = 0) creates
+// it for g_d devices and exports a shareable handle; every member imports it, adds its device,
+// binds its own NVLS memory and maps the multicast range.  Every rank's NVLS memory is also
+// exported and mapped by every peer (unicast), so phases NOT run in the switch read peers
+// directly, as in the cudaIpc path.  Four collective rounds, each an all-gather of a fixed-size
+// blob done by the caller (the Python binding uses the process group):
+//   prepare -> attach -> bind -> commit.
+// Any failure on any rank (no multicast support, no fabric manager, one GPU, ...) makes every
+// rank fall back to the direct P2P phases: commit enables NVLS only when all ranks succeeded.
+//
+// Driver entry points are resolved at run time (cudaGetDriverEntryPoint), so libddl keeps
+// linking only the static CUDA runtime.  Handle exchange: CU_MEM_HANDLE_TYPE_FABRIC when the
+// allocation supports it (a 64-byte blob), else POSIX file descriptors passed with
+// pidfd_open / pidfd_getfd (same node, same user).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cstdint>
+#include <cstring>
+
+#ifndef SYS_pidfd_open
+#define SYS_pidfd_open 434
+#endif
+#ifndef SYS_pidfd_getfd
+#define SYS_pidfd_getfd 438
+#endif
+
+namespace ddl {
+namespace nvls {
+
+struct Api {
+  bool ok = false;
+  CUresult (*getAttr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+  CUresult (*mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+  CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+  CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                        unsigned long long) = nullptr;
+  CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+  CUresult (*mcGranularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+  CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) =
+      nullptr;
+  CUresult (*memGranularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*memExport)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long) =
+      nullptr;
+  CUresult (*memImport)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
+  CUresult (*addrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*addrFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*memUnmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*memRelease)(CUmemGenericAllocationHandle) = nullptr;
+};
+
+template <typename F>
+inline bool resolve(const char* name, F* fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+      !p) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  *fn = reinterpret_cast<F>(p);
+  return true;
+}
+
+inline Api& api() {
+  static Api a = [] {
+    Api x;
+    x.ok = resolve("cuDeviceGetAttribute", &x.getAttr) && resolve("cuMulticastCreate", &x.mcCreate) &&
+           resolve("cuMulticastAddDevice", &x.mcAddDevice) && resolve("cuMulticastBindMem", &x.mcBindMem) &&
+           resolve("cuMulticastUnbind", &x.mcUnbind) && resolve("cuMulticastGetGranularity", &x.mcGranularity) &&
+           resolve("cuMemCreate", &x.memCreate) && resolve("cuMemGetAllocationGranularity", &x.memGranularity) &&
+           resolve("cuMemExportToShareableHandle", &x.memExport) &&
+           resolve("cuMemImportFromShareableHandle", &x.memImport) && resolve("cuMemAddressReserve", &x.addrReserve) &&
+           resolve("cuMemAddressFree", &x.addrFree) && resolve("cuMemMap", &x.memMap) &&
+           resolve("cuMemUnmap", &x.memUnmap) && resolve("cuMemSetAccess", &x.setAccess) &&
+           resolve("cuMemRelease", &x.memRelease);
+    return x;
+  }();
+  return a;
+}
+
+constexpr uint32_t kBlobMagic = 0xDD1A7715u;
+enum Status : int32_t { kOk = 0, kNoApi = 1, kNoMulticast = 2, kAllocFailed = 3, kCreateFailed = 4,
+                        kImportFailed = 5, kAddFailed = 6, kBindFailed = 7, kMapFailed = 8, kPeerFailed = 9 };
+
+// One rank's contribution to a round (all-gathered by the caller, nranks * sizeof(Blob)).
+struct Blob {
+  uint32_t magic;
+  int32_t rank;
+  int32_t status;  // Status of this rank after the round
+  int32_t htype;   // CUmemAllocationHandleType used (FABRIC or POSIX_FILE_DESCRIPTOR)
+  int32_t pid;
+  int32_t phys_fd;
+  uint64_t bytes;  // rounded NVLS bytes per rank (all ranks equal)
+  int32_t mc_fd[kMaxDims];
+  CUmemFabricHandle phys_fab;
+  CUmemFabricHandle mc_fab[kMaxDims];
+};
+
+// Per-communicator state.
+struct State {
+  int stage = 0;  // 0 none, 1 prepared, 2 attached, 3 bound, 4 ready
+  int dev = 0;
+  CUmemAllocationHandleType htype = CU_MEM_HANDLE_TYPE_NONE;
+  size_t bytes = 0;
+  CUmemGenericAllocationHandle phys = 0;
+  int phys_fd = -1;
+  char* uc[kMaxRanks] = {};                        // unicast mappings: own (uc[rank]) and peers'
+  CUmemGenericAllocationHandle peer_phys[kMaxRanks] = {};
+  CUmemGenericAllocationHandle mc[kMaxDims] = {};  // multicast object of my dim-d group
+  int mc_fd[kMaxDims];
+  bool mc_added[kMaxDims] = {};
+  bool mc_bound[kMaxDims] = {};
+  char* mcva[kMaxDims] = {};
+  int mask = 0;  // dims running in the switch (after commit)
+  State() {
+    for (int d = 0; d < kMaxDims; ++d) mc_fd[d] = -1;
+  }
+};
+
+// Import a peer's shareable handle: fabric blob, or (pid, fd) through pidfd_getfd.
+inline CUresult import_handle(CUmemGenericAllocationHandle* h, CUmemAllocationHandleType ht, int pid, int fd,
+                              const CUmemFabricHandle* fab) {
+  Api& a = api();
+  if (ht == CU_MEM_HANDLE_TYPE_FABRIC) return a.memImport(h, const_cast<CUmemFabricHandle*>(fab), ht);
+  const int pfd = (int)syscall(SYS_pidfd_open, pid, 0);
+  if (pfd < 0) return CUDA_ERROR_INVALID_HANDLE;
+  const int local = (int)syscall(SYS_pidfd_getfd, pfd, fd, 0);
+  close(pfd);
+  if (local < 0) return CUDA_ERROR_INVALID_HANDLE;
+  CUresult r = a.memImport(h, reinterpret_cast<void*>((uintptr_t)local), ht);
+  close(local);
+  return r;
+}
+
+inline CUresult map_rw(CUmemGenericAllocationHandle h, size_t bytes, size_t align, int dev, char** va) {
+  Api& a = api();
+  CUdeviceptr p = 0;
+  CUresult r = a.addrReserve(&p, bytes, align, 0, 0);
+  if (r != CUDA_SUCCESS) return r;
+  r = a.memMap(p, bytes, 0, h, 0);
+  if (r != CUDA_SUCCESS) {
+    a.addrFree(p, bytes);
+    return r;
+  }
+  CUmemAccessDesc acc;
+  std::memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  r = a.setAccess(p, bytes, &acc, 1);
+  if (r != CUDA_SUCCESS) {
+    a.memUnmap(p, bytes);
+    a.addrFree(p, bytes);
+    return r;
+  }
+  *va = reinterpret_cast<char*>(p);
+  return CUDA_SUCCESS;
+}
+
+inline void unmap(char** va, size_t bytes) {
+  if (*va) {
+    api().memUnmap((CUdeviceptr)*va, bytes);
+    api().addrFree((CUdeviceptr)*va, bytes);
+    *va = nullptr;
+  }
+}
+
+// Release everything (any stage); safe to call twice.
+inline void teardown(State& s, const Topo& t, int rank) {
+  if (!api().ok) return;
+  for (int d = 0; d < kMaxDims; ++d) {
+    unmap(&s.mcva[d], s.bytes);
+    if (s.mc_bound[d]) api().mcUnbind(s.mc[d], s.dev, 0, s.bytes);
+    s.mc_bound[d] = false;
+    if (s.mc[d]) api().memRelease(s.mc[d]);
+    s.mc[d] = 0;
+    if (s.mc_fd[d] >= 0) close(s.mc_fd[d]);
+    s.mc_fd[d] = -1;
+    s.mc_added[d] = false;
+  }
+  for (int m = 0; m < t.P; ++m) {
+    unmap(&s.uc[m], s.bytes);
+    if (m != rank && s.peer_phys[m]) api().memRelease(s.peer_phys[m]);
+    s.peer_phys[m] = 0;
+  }
+  if (s.phys) api().memRelease(s.phys);
+  s.phys = 0;
+  if (s.phys_fd >= 0) close(s.phys_fd);
+  s.phys_fd = -1;
+  s.mask = 0;
+  s.stage = 0;
+}
+
+}  // namespace nvls
+}  // namespace ddl

@@ -68,6 +68,12 @@ def _load() -> ctypes.CDLL:
         "ddl_connect": (c_int, [c_void, c_void]),
         "ddl_buffer": (c_int, [c_void, pp, ctypes.POINTER(c_size)]),
         "ddl_peer_buffer": (c_int, [c_void, c_int, pp, ctypes.POINTER(c_size)]),
+        "ddl_nvls_blob_size": (c_size, []),
+        "ddl_nvls_prepare": (c_int, [c_void, c_size, c_void]),
+        "ddl_nvls_attach": (c_int, [c_void, c_void, c_void]),
+        "ddl_nvls_bind": (c_int, [c_void, c_void, c_void]),
+        "ddl_nvls_commit": (c_int, [c_void, c_void]),
+        "ddl_nvls_buffer": (c_int, [c_void, pp, ctypes.POINTER(c_size), ip]),
         "ddl_allreduce": (c_int, [c_void, c_void, c_size, c_int, c_int, c_void]),
         "ddl_allreduce_many": (c_int, [c_void, pp, ctypes.POINTER(c_size), c_int, c_int, c_int, c_void]),
         "ddl_reduce_scatter": (c_int, [c_void, c_void, c_void, c_size, c_int, c_int, c_void]),
@@ -244,7 +250,8 @@ class Comm:
     every rank of ``group`` calls ``Comm(dims, ...)``; cudaIpc handles are exchanged with
     ``all_gather_object`` on the (gloo or NCCL) process group -- bootstrap only."""
 
-    def __init__(self, dims=None, group=None, max_bytes: int = 256 << 20, device: int | None = None):
+    def __init__(self, dims=None, group=None, max_bytes: int = 256 << 20, device: int | None = None,
+                 nvls_bytes: int | None = None):
         torch = _torch()
         import torch.distributed as dist
         self.group = group
@@ -267,6 +274,51 @@ class Comm:
         n = ctypes.c_size_t()
         _check(_lib.ddl_buffer(self.h, ctypes.byref(p), ctypes.byref(n)), "ddl_buffer")
         self.buffer_ptr, self.buffer_bytes = p.value, n.value
+        # NVLS phases (ddl_nvls_*): requested with nvls_bytes or DDL_NVLS_BYTES; falls back
+        # to the direct phases on every rank if any rank cannot take part
+        self.nvls_ptr, self.nvls_bytes, self.nvls_mask, self.nvls_status = 0, 0, 0, "off"
+        nb = nvls_bytes if nvls_bytes is not None else int(os.environ.get("DDL_NVLS_BYTES", "0"))
+        if nb > 0 and self.nranks > 1:
+            self._nvls_setup(nb)
+
+    def _nvls_setup(self, nbytes: int) -> None:
+        import torch.distributed as dist
+        bs = _lib.ddl_nvls_blob_size()
+
+        def gather(blob):
+            allb = [None] * self.nranks
+            dist.all_gather_object(allb, bytes(blob.raw), group=self.group)
+            return ctypes.create_string_buffer(b"".join(allb), bs * self.nranks)
+
+        mine = ctypes.create_string_buffer(bs)
+        _check(_lib.ddl_nvls_prepare(self.h, nbytes, mine), "ddl_nvls_prepare")
+        allb = gather(mine)
+        for step, fn in (("attach", _lib.ddl_nvls_attach), ("bind", _lib.ddl_nvls_bind)):
+            mine = ctypes.create_string_buffer(bs)
+            _check(fn(self.h, allb, mine), f"ddl_nvls_{step}")
+            allb = gather(mine)
+        statuses = [int.from_bytes(allb.raw[r * bs + 8:r * bs + 12], "little", signed=True) for r in range(self.nranks)]
+        code = _lib.ddl_nvls_commit(self.h, allb)
+        if code == SUCCESS:
+            p, n, m = ctypes.c_void_p(), ctypes.c_size_t(), ctypes.c_int()
+            _check(_lib.ddl_nvls_buffer(self.h, ctypes.byref(p), ctypes.byref(n), ctypes.byref(m)), "ddl_nvls_buffer")
+            self.nvls_ptr, self.nvls_bytes, self.nvls_mask, self.nvls_status = p.value, n.value, m.value, "on"
+        elif code == ERR_UNSUPPORTED:
+            self.nvls_status = f"fallback (per-rank setup status {statuses}: see ddl_nvls.h Status)"
+        else:
+            _check(code, "ddl_nvls_commit")
+
+    def nvls_buffer(self, count: int, dtype, offset_bytes: int = 0):
+        """A tensor view of this rank's NVLS buffer (same offset on every rank): all-reduces
+        of it run the NVLS phases.  Raises if NVLS is off (see ``nvls_status``)."""
+        torch = _torch()
+        if not self.nvls_ptr:
+            raise DDLError(ERR_UNSUPPORTED, f"NVLS {self.nvls_status}")
+        esz = torch.tensor([], dtype=dtype).element_size()
+        if offset_bytes % 256 or offset_bytes + count * esz > self.nvls_bytes:
+            raise DDLError(ERR_TOO_LARGE, "view outside the NVLS buffer")
+        full = _tensor_from_ptr(self.nvls_ptr, self.nvls_bytes, self.device)
+        return full[offset_bytes:offset_bytes + count * esz].view(dtype)
 
     def buffer(self, count: int, dtype, offset_bytes: int = 0):
         """A torch tensor view of the symmetric zero-copy buffer (same offset on every rank)."""
@@ -290,6 +342,11 @@ class Comm:
         full = _tensor_from_ptr(p.value, n.value, self.device)
         return full[offset_bytes:offset_bytes + count * esz].view(dtype)
 
+    def _zero_copy(self, ptr: int, nbytes: int) -> bool:
+        """Inside the symmetric buffer or the NVLS buffer (read by peers in place)."""
+        return (self.buffer_ptr <= ptr and ptr + nbytes <= self.buffer_ptr + self.buffer_bytes) or \
+            (bool(self.nvls_ptr) and self.nvls_ptr <= ptr and ptr + nbytes <= self.nvls_ptr + self.nvls_bytes)
+
     def all_reduce(self, t, op: str = "sum", stream=None):
         """In-place all-reduce.  A tensor inside the symmetric buffer is reduced zero-copy;
         any other tensor larger than the staging workspace is reduced in workspace-sized
@@ -298,7 +355,7 @@ class Comm:
         _require_cuda(t)
         dt = DTYPE_CODES[dtype_name(t)]
         nbytes = t.numel() * t.element_size()
-        inside = self.buffer_ptr <= t.data_ptr() and t.data_ptr() + nbytes <= self.buffer_ptr + self.buffer_bytes
+        inside = self._zero_copy(t.data_ptr(), nbytes)
         piece = (self.buffer_bytes // t.element_size()) // 256 * 256
         if inside or nbytes <= self.buffer_bytes or piece == 0:
             _check(_lib.ddl_allreduce(self.h, t.data_ptr(), t.numel(), dt, OP_CODES[op],
@@ -325,7 +382,7 @@ class Comm:
             if dtype_name(t) != dt:
                 raise DDLError(ERR_INVALID_ARGUMENT, "all_reduce_many: mixed dtypes")
             nbytes = t.numel() * t.element_size()
-            inside = self.buffer_ptr <= t.data_ptr() and t.data_ptr() + nbytes <= self.buffer_ptr + self.buffer_bytes
+            inside = self._zero_copy(t.data_ptr(), nbytes)
             if not inside and nbytes > self.buffer_bytes:
                 self.all_reduce(t, op, stream)   # staged in workspace-sized pieces
             else:
@@ -513,11 +570,11 @@ class Loopback:
         return _lib.ddl_ctas_for(self.h, count, DTYPE_CODES[dtype])
 
     def trace(self):
-        """[nranks][cmax][40] globaltimer stamps of the last call (DDL_TRACE=1 at init)."""
+        """[nranks][cmax][128] globaltimer (slot 127: the SM id) stamps of the last call (DDL_TRACE=1 at init)."""
         import numpy as np
         torch = _torch()
         cmax = 4 * torch.cuda.get_device_properties(self.device).multi_processor_count
-        out = np.zeros((self.nranks, cmax, 40), dtype=np.uint64)
+        out = np.zeros((self.nranks, cmax, 128), dtype=np.uint64)
         _check(_lib.ddl_debug_trace(self.h, out.ctypes.data, out.nbytes), "ddl_debug_trace")
         return out
 

@@ -26,13 +26,13 @@ bufs = [[torch.from_numpy(host[r][b]).cuda() for r in range(P)] for b in range(l
 for _ in range(6):
     lb.all_reduce_many(bufs, "avg")
 torch.cuda.synchronize()
-tr = lb.trace().astype(np.int64)          # [P][cmax][40]
+tr = lb.trace().astype(np.int64)          # [P][cmax][128]
 C = 37
 tr = tr[:, :C, :]
 t0 = tr[:, :, 0].min()
 us = lambda x: x / 1e3                    # noqa: E731
-nev = (tr[:, :, 1:39] > 0).sum(axis=2)    # events recorded per CTA -> its channel's bucket-waves
-end_ev = [tr[r, c, 1:39][tr[r, c, 1:39] > 0].max() for r in range(P) for c in range(C)]
+nev = (tr[:, :, 1:127] > 0).sum(axis=2)    # events recorded per CTA -> its channel's bucket-waves
+end_ev = [tr[r, c, 1:127][tr[r, c, 1:127] > 0].max() for r in range(P) for c in range(C)]
 print(f"grouped step, dims {a.dims}: total {us(max(end_ev) - t0):.1f} us")
 for ne in sorted(set(nev.ravel().tolist())):
     sel = nev == ne

@@ -25,7 +25,7 @@ for k in range(a.calls + 2):
         continue
     d = (tr[:, :, 3] - tr[:, :, 2]).ravel() / 1e3   # RS0 duration per CTA (us)
     durs.append(d)
-    sms = tr[:, :, 39].ravel()
+    sms = tr[:, :, 127].ravel()
 D = np.array(durs)
 print("per-call RS0 min/med/max:", [(round(x.min(), 1), round(np.median(x), 1), round(x.max(), 1)) for x in D])
 cc = np.corrcoef(D)

@@ -89,6 +89,30 @@ def _rank_main(rank, world, port, q, env, dims):
         torch.cuda.synchronize()
         res["grouped"] = tuple(same_bits(to_host(v), oracle.allreduce(b, dims, "float32", "avg")[rank])
                                for v, b in zip(views, gb))
+        # NVLS phases (DDL_NVLS_BYTES at init): on one GPU the multicast setup must fall back on
+        # every rank (everything above ran on the direct phases); where it is on (an NVSwitch
+        # box with one GPU per process), buffers in the NVLS region are checked: int32 exact,
+        # fp32 within the any-order bound of the exact sum (oracle.fold_error_bound)
+        res["nvls"] = (comm.nvls_status == "on" or comm.nvls_status.startswith("fallback")
+                       or "DDL_NVLS_BYTES" not in env,)
+        if comm.nvls_status == "on":
+            ok = []
+            for dtype, op in (("int32", "sum"), ("float32", "avg"), ("bfloat16", "avg")):
+                kind = "fullrange" if dtype == "int32" else "normal"
+                n = 1 << 20
+                bufs = si.rank_buffers(dtype, kind, n, world, seed=77)
+                t = comm.nvls_buffer(n, to_dev(bufs[0][:1], dtype).dtype)
+                t.copy_(to_dev(bufs[rank], dtype))
+                comm.all_reduce(t, op)
+                torch.cuda.synchronize()
+                got = to_host(t)
+                if dtype == "int32":
+                    ok.append(same_bits(got, oracle.naive_sum(bufs, "int32")))
+                else:
+                    y = oracle.bf16_to_f32(got) if dtype == "bfloat16" else got
+                    s64, bound = oracle.fold_error_bound(bufs, dims, dtype, op)
+                    ok.append(bool(np.all(np.abs(y.astype(np.float64) - s64) <= bound)))
+            res["nvls"] = tuple(ok)
         res["err"] = comm.async_error()
         comm.finalize()
     except Exception as e:  # report, don't hang the parent
@@ -100,8 +124,10 @@ def _rank_main(rank, world, port, q, env, dims):
 @pytest.mark.timeout(400)
 @pytest.mark.parametrize("world,dims,env", [(2, [2], {}), (2, [2], {"DDL_TMA_MIN_SLICE_BYTES": "0"}),
                                             (4, [2, 2], {"DDL_TMA_MIN_SLICE_BYTES": "0"}),
-                                            (8, [4, 2], {})],
-                         ids=["2-default", "2-tma", "4-2x2-tma", "8-2x4"])
+                                            (8, [4, 2], {}),
+                                            (2, [2], {"DDL_NVLS_BYTES": str(8 << 20)}),
+                                            (4, [2, 2], {"DDL_NVLS_BYTES": str(8 << 20)})],
+                         ids=["2-default", "2-tma", "4-2x2-tma", "8-2x4", "2-nvls", "4-2x2-nvls"])
 def test_processes_ipc_one_gpu(world, dims, env):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -122,5 +148,5 @@ def test_processes_ipc_one_gpu(world, dims, env):
     for r in range(world):
         assert "exc" not in out[r], out[r]
         assert out[r]["err"] == 0
-        for dtype in ("float32", "int32", "bfloat16", "ll", "big", "registered", "grouped"):
+        for dtype in ("float32", "int32", "bfloat16", "ll", "big", "registered", "grouped", "nvls"):
             assert all(out[r][dtype]), (r, dtype)

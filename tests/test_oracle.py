@@ -592,3 +592,68 @@ def test_local_reduce():
     b = si.rank_buffers("bfloat16", "normal", 1000, 4)
     want = oracle.bf16_round(oracle.naive_sum(b, "bfloat16"))
     assert np.array_equal(oracle.local_reduce(b, "bfloat16"), want)
+
+
+# --------------------------------------------------------------------------- NVLS phases (NEXT-1)
+
+def _exact_fraction_sum(vals):
+    from fractions import Fraction
+    return sum((Fraction(float(v)) for v in vals), Fraction(0))
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_nvls_int32_exact(P):
+    """int32 NVLS phases: every fold order reaches the exact sum mod 2^32 (bit-exact pin)."""
+    bufs = si.rank_buffers("int32", "fullrange", 777, P)
+    want = oracle.naive_sum(bufs, "int32")
+    for dims in factorisations(P):
+        live = [d for d, g in enumerate(dims) if g > 1]
+        for nv in ([], live, live[:1]):
+            out = oracle.allreduce(bufs, dims, "int32", "sum", nvls_dims=nv)
+            assert all(np.array_equal(y, want) for y in out), (dims, nv)
+
+
+def test_nvls_switch_sum_correctly_rounded_flat():
+    """dims [P] with its one phase in the switch: the oracle's admissible result is the
+    exact sum rounded once to binary32 -- checked with exact rational arithmetic
+    (fractions) on every element: |y - s| <= 2^-24 |s| (half an ulp)."""
+    P = 8
+    bufs = si.rank_buffers("float32", "normal", 400, P)
+    y = oracle.allreduce(bufs, [P], "float32", "sum", nvls_dims=[0])[0]
+    for e in range(400):
+        s = _exact_fraction_sum([b[e] for b in bufs])
+        assert abs(float(y[e]) - float(s)) <= 2.0 ** -24 * abs(float(s)) * (1 + 1e-9), e
+
+
+def test_nvls_two_member_phases_equal_direct():
+    """A 2-member phase has only one fold (a + b == b + a exactly, rounded once), so an NVLS
+    [2, 2, 2] all-reduce equals the direct one bit for bit (fp32 sum and avg)."""
+    bufs = si.rank_buffers("float32", "normal", 1000, 8)
+    for op in ("sum", "avg"):
+        a = oracle.allreduce(bufs, [2, 2, 2], "float32", op)
+        b = oracle.allreduce(bufs, [2, 2, 2], "float32", op, nvls_dims=[0, 1, 2])
+        assert all(same_bits(x, y) for x, y in zip(a, b))
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+@pytest.mark.parametrize("P", [2, 4, 8, 16])
+def test_fold_error_bound_holds_for_every_order(dtype, P):
+    """fold_error_bound is a valid bound for the direct order, the switch order on any subset
+    of dims, and a brute-force fold in REVERSED member order (another admissible tree); and it
+    is not vacuous: fp32 stays below north_star's 1e-6 componentwise gate for P <= 16."""
+    bufs = si.rank_buffers(dtype, "normal", 3000, P)
+    for dims in factorisations(P):
+        for op in ("sum", "avg"):
+            s, bound = oracle.fold_error_bound(bufs, dims, dtype, op)
+            live = [d for d, g in enumerate(dims) if g > 1]
+            for nv in ([], live, live[-1:]):
+                y = oracle.allreduce(bufs, dims, dtype, op, nvls_dims=nv)[0]
+                yf = oracle.bf16_to_f32(y) if dtype == "bfloat16" else y
+                assert np.all(np.abs(yf.astype(np.float64) - s) <= bound), (dims, op, nv)
+            rev = oracle.allreduce(bufs[::-1], dims, dtype, op)[0]
+            rf = oracle.bf16_to_f32(rev) if dtype == "bfloat16" else rev
+            assert np.all(np.abs(rf.astype(np.float64) - s) <= bound), (dims, op, "reversed")
+            _, a64 = oracle.exact_sum_f64(bufs, dtype)
+            if dtype == "float32" and (op == "sum" or P <= 8):   # avg adds 3u|s|/P for the multiply
+                mag = a64 / P if op == "avg" else a64
+                assert np.all(bound <= 1e-6 * mag + 1e-30)
