@@ -180,7 +180,7 @@ def d_channels(ctx, out):
     host = bench.resnet50_set(ctx.rank)
     S = sum(h.size for h in host) * 4
     for ch in ("1", "2", "3", "4"):
-        for hints in ("15", "0"):
+        for hints in ("47", "15", "0"):
             comm = ctx.comm(ddl.parse_dims(spec), {"DDL_CHANNELS": ch, "DDL_L2_HINTS": hints}, S + 8 * MIB)
             off, views = 0, []
             for h in host:

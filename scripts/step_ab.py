@@ -76,7 +76,14 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) / 20)
-        print(f"{cfg or 'default':60s} ms/step {statistics.median(ts):.4f} (min {min(ts):.4f}) ok={ok}", flush=True)
+        # value check again after the timed calls (learned state, if any, now in use)
+        a = [[t.clone() for t in bk] for bk in bufs]
+        lb.all_reduce_many(a, "avg")
+        torch.cuda.synchronize()
+        ok2 = all(torch.equal(x.view(torch.int32), y.view(torch.int32)) for bx, by in zip(a, ref) for x, y in zip(bx, by))
+        del a
+        print(f"{cfg or 'default':60s} ms/step {statistics.median(ts):.4f} (min {min(ts):.4f}) ok={ok} ok_after={ok2} "
+              f"err={lb.async_error()}", flush=True)
         del g
         lb.finalize()
 

@@ -73,3 +73,16 @@ vals = sorted((np.mean(v), s) for s, v in smb.items())
 print("slowest SMs (mean busy us):", [(s, round(m / 1e3, 1)) for m, s in vals[-8:]])
 print("fastest SMs (mean busy us):", [(s, round(m / 1e3, 1)) for m, s in vals[:8]])
 lb.finalize()
+# chain analysis: a slice chain = the same CTA index on every rank; its phase pace is set by
+# its slowest member.  Compare with chains formed from SMs of neighbouring ids.
+b = busy_runs[-1]
+chain_max = b.max(axis=0)
+print(f"chains by CTA index: max-member busy min {chain_max.min() / 1e3:.1f} med {np.median(chain_max) / 1e3:.1f} "
+      f"max {chain_max.max() / 1e3:.1f} us; mean member busy {b.mean() / 1e3:.1f} us")
+sm_mean = {s: np.mean(v) for s, v in smb.items()}
+ids = sorted(sm_mean)
+grp = [ids[i:i + 4] for i in range(0, len(ids), 4)]
+gm = np.array([max(sm_mean[s] for s in g) for g in grp])
+print(f"hypothetical chains of 4 neighbouring SMs: slowest-SM busy min {gm.min() / 1e3:.1f} med {np.median(gm) / 1e3:.1f} "
+      f"max {gm.max() / 1e3:.1f} us; harmonic balance -> {len(gm) / np.sum(1.0 / gm) / 1e3:.1f} us")
+print("per-SM mean busy (us) by SM id:", [round(sm_mean[s] / 1e3) for s in ids])
