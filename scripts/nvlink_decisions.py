@@ -20,6 +20,9 @@ One CSV per decision, rows `decision,label,P,dims,bytes,us,busbw_GBs,pct_900`:
 * channels    -- the bench step (5 ResNet-50 buckets, grouped) with DDL_CHANNELS 1-4 and L2
                  hints on (15) / off (0).
 * waves       -- hierarchical calls in 1 / 2 / 4 / 8 waves (DDL_WAVES) at 32-256 MiB.
+* nvls        -- the NVLS phases (multimem, DDL_NVLS_BYTES) on every live dim and on each
+                 dim alone (DDL_NVLS_DIMS), 1-256 MiB; a row UNAVAILABLE (with the setup
+                 status) where the box cannot create multicast objects.
 * barrier_rtt -- the .sys barrier round trip over NVSwitch: tiny hierarchical calls (one
                  16-B vector per block) on dims with 1, 2, 3 live dims (3, 5, 7 barriers);
                  the slope is the cost of one barrier.
@@ -213,8 +216,45 @@ def d_barrier_rtt(ctx, out):
         comm.finalize()
 
 
+def d_nvls(ctx, out):
+    """NVLS phases (DDL_NVLS_BYTES): every live dim in the switch, and each dim alone
+    (DDL_NVLS_DIMS), against the direct phases on the same sizes.  fp32 results of switch
+    phases are checked against the any-order bound on x_r = r + 1 (exact integers: every
+    order gives P(P+1)/2), so the value gate holds here too."""
+    P = ctx.world
+    sizes = [S for S in (MIB << j for j in range(0, 9, 2)) if S <= ctx.args.max_bytes] or [MIB]
+    for spec in dict.fromkeys([default_dims(P), str(P)]):
+        dims = ddl.parse_dims(spec)
+        live = [d for d, g in enumerate(dims) if g > 1]
+        masks = [None] + ([str(1 << d) for d in live] if len(live) > 1 else [])
+        for mask in masks:
+            env = {"DDL_NVLS_BYTES": str(max(sizes) + MIB)}
+            if mask:
+                env["DDL_NVLS_DIMS"] = mask
+            comm = ctx.comm(dims, env, MIB)
+            label = f"nvls-mask{mask or 'all'}"
+            if comm.nvls_status != "on":
+                if ctx.rank == 0:
+                    print(f"nvls,{label},{P},{spec},0,UNAVAILABLE,,{comm.nvls_status[:60]}", file=out, flush=True)
+                comm.finalize()
+                continue
+            comm.set_algo(ddl.ALGO_HIER, 0)
+            for S in sizes:
+                n = S // 4
+                t = comm.nvls_buffer(n, torch.float32)
+                t.fill_(float(ctx.rank + 1))
+                comm.all_reduce(t, "sum")
+                torch.cuda.synchronize()
+                ok = bool((t == P * (P + 1) // 2).all())
+                us = None if ctx.max_over_ranks(0.0 if ok else 1.0) else \
+                    ctx.max_over_ranks(time_graph(lambda: comm.all_reduce(t, "sum"),
+                                                  ctx.args.iters or max(3, min(200, int(2e9 // S)))))
+                row(ctx, out, "nvls", label, spec, S, us)
+            comm.finalize()
+
+
 DECISIONS = {"crossover": d_crossover, "barriers": d_barriers, "tma": d_tma, "channels": d_channels,
-             "waves": d_waves, "barrier_rtt": d_barrier_rtt}
+             "waves": d_waves, "barrier_rtt": d_barrier_rtt, "nvls": d_nvls}
 
 
 def main():

@@ -20,5 +20,6 @@ if [ "${DDL_BENCH_SAME_GPU:-0}" != "1" ]; then
     > "$OUT/sweep_nonvls.log" 2>&1
   NCCL_DEBUG=INFO NCCL_DEBUG_SUBSYS=INIT,TUNING timeout 600 $RUN bench.py --gpus $N --steps 20 --warmup 5 \
     > "$OUT/bench_P$N.log" 2>&1
+  OUT="$OUT/nvl" bash scripts/ncu_nvlink.sh $N > "$OUT/ncu_nvlink.log" 2>&1 || true
 fi
 ls -la "$OUT"

@@ -1,5 +1,5 @@
 set -x
-TAG=${TAG:-r01_v17}
+TAG=${TAG:-r02_v1}
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q --timeout 600 2>&1 | tail -4 > gpurun_out/${TAG}_pytest_gpu.txt
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.txt 2>&1
