@@ -123,7 +123,8 @@ ddl_result_t ddl_plan_traffic(size_t count, ddl_dtype_t dtype, int nranks, const
                               int rank, uint64_t* rs_out, uint64_t* ag_out);
 
 /* ------------------------------------------------------------------ multi-process comm */
-/* One process per GPU.  Bootstrap: ddl_init -> ddl_export_handle -> (caller all-gathers
+/* One process per GPU (the paper's MPI-like `rank`, §2.1; dims as SPEC S:L264-270:
+ * innermost first, prod(dims) == nranks, g_d >= 1).  Bootstrap: ddl_init -> ddl_export_handle -> (caller all-gathers
  * the handles, e.g. torch.distributed.all_gather_object) -> ddl_connect(all, rank order).
  * The handle bytes carry a cudaIpc memory handle of this rank's flag+workspace block. */
 
@@ -183,7 +184,10 @@ ddl_result_t ddl_register_export(ddl_comm_t comm, void* ptr, size_t bytes, void*
 ddl_result_t ddl_register_connect(ddl_comm_t comm, void* ptr, const void* all_handles, int* reg_id);
 ddl_result_t ddl_deregister(ddl_comm_t comm, int reg_id);
 
-/* In-place all-reduce of buf[0, count).  buf inside ddl_buffer() or a registered buffer:
+/* In-place all-reduce of buf[0, count) -- "one all-reduce operation decomposed into a series
+ * of reduce-scatter and all-gather patterns in a topology-aware fashion" (§2.1):
+ * RS phases innermost dim first, AG phases outermost first; avg multiplies
+ * the fully reduced fp32 value by fl32(1/P) once (DESIGN reading 5).  buf inside ddl_buffer() or a registered buffer:
  * zero-copy; any other device buffer: staged through the workspace (count * size <=
  * max_bytes). */
 ddl_result_t ddl_allreduce(ddl_comm_t comm, void* buf, size_t count, ddl_dtype_t dtype,
@@ -204,14 +208,16 @@ ddl_result_t ddl_allreduce(ddl_comm_t comm, void* buf, size_t count, ddl_dtype_t
 ddl_result_t ddl_allreduce_many(ddl_comm_t comm, void* const* bufs, const size_t* counts, int nbufs,
                                 ddl_dtype_t dtype, ddl_op_t op, void* stream);
 
-/* NCCL layout: sendbuf holds nranks * recvcount elements; rank r receives elements
+/* The reduce-scatter half of the decomposition alone.
+ * NCCL layout: sendbuf holds nranks * recvcount elements; rank r receives elements
  * [r*recvcount, (r+1)*recvcount) of the reduced vector.  sendbuf is not modified.
  * The partial sums live in the workspace: nranks * recvcount * size <= max_bytes.  A
  * sendbuf in the symmetric / a registered buffer is read in place (no copy-in). */
 ddl_result_t ddl_reduce_scatter(ddl_comm_t comm, const void* sendbuf, void* recvbuf, size_t recvcount,
                                 ddl_dtype_t dtype, ddl_op_t op, void* stream);
 
-/* Rank r's sendcount elements land at [r*sendcount, (r+1)*sendcount) of every rank's
+/* The all-gather half of the decomposition alone.
+ * Rank r's sendcount elements land at [r*sendcount, (r+1)*sendcount) of every rank's
  * recvbuf (nranks * sendcount elements).  A recvbuf in the symmetric / a registered buffer
  * is gathered into in place; otherwise staged through the workspace (<= max_bytes). */
 ddl_result_t ddl_allgather(ddl_comm_t comm, const void* sendbuf, void* recvbuf, size_t sendcount,
@@ -270,6 +276,10 @@ ddl_result_t ddl_finalize(ddl_comm_t comm);
  * "peer" pointers that are local.  Used by the parity tests and the 1-GPU benchmark. */
 
 ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, int ndims, int cuda_device);
+/* The same under SURVEY 8(b)'s name and argument list (max_bytes is unused: loopback calls
+ * work on the caller's buffers in place; reduce-scatter grows its workspace on demand). */
+ddl_result_t ddl_init_loopback(ddl_comm_t* comm, int nranks, const int* dims, int ndims, int cuda_device,
+                               size_t max_bytes);
 
 /* bufs: host array of nranks device pointers (distinct, 16-B aligned, count elements
  * each); in place. */

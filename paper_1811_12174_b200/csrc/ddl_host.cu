@@ -1413,6 +1413,12 @@ ddl_result_t ddl_finalize(ddl_comm_t c) {
 }
 
 // ------------------------------------------------------------------ loopback
+ddl_result_t ddl_init_loopback(ddl_comm_t* comm, int nranks, const int* dims, int ndims, int cuda_device,
+                               size_t max_bytes) {
+  (void)max_bytes;
+  return ddl_loopback_init(comm, nranks, dims, ndims, cuda_device);
+}
+
 ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, int ndims, int cuda_device) {
   if (!comm) return DDL_ERR_INVALID_ARGUMENT;
   *comm = nullptr;

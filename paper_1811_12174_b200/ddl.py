@@ -94,6 +94,7 @@ def _load() -> ctypes.CDLL:
         "ddl_debug_trace": (c_int, [c_void, c_void, c_size]),
         "ddl_finalize": (c_int, [c_void]),
         "ddl_loopback_init": (c_int, [pp, c_int, ip, c_int, c_int]),
+        "ddl_init_loopback": (c_int, [pp, c_int, ip, c_int, c_int, c_size]),
         "ddl_group_allreduce": (c_int, [c_void, pp, c_size, c_int, c_int, c_void]),
         "ddl_group_allreduce_many": (c_int, [c_void, pp, ctypes.POINTER(c_size), c_int, c_int, c_int, c_void]),
         "ddl_group_reduce_scatter": (c_int, [c_void, pp, pp, c_size, c_int, c_int, c_void]),

@@ -377,3 +377,34 @@ def test_config4_bf16_gate_every_element(spec):
     print(f"\nconfig4 bf16 {spec}: max |y - s/P| / (sum|x|/P) over {n} elements = {worst:.4e}")
     assert worst <= 1e-2, worst
     lb.finalize()
+
+
+def test_slice_over_1gib_cut_into_waves():
+    """per-CTA slice fields are 32-bit.  With one CTA per rank (DDL_CTAS=1) and a
+    message whose per-CTA slice exceeds 1 GiB, the call is cut into waves (or refused with
+    DDL_ERR_TOO_LARGE), never silently wrapped: every element of a 2-rank int32 all-reduce
+    of 2^29 + 64 elements per rank equals the closed form."""
+    old = os.environ.get("DDL_CTAS")
+    os.environ["DDL_CTAS"] = "1"
+    try:
+        lb = ddl.Loopback(2, [2])
+    finally:
+        if old is None:
+            os.environ.pop("DDL_CTAS", None)
+        else:
+            os.environ["DDL_CTAS"] = old
+    lb.set_algo(ddl.ALGO_HIER, 0)
+    n = (1 << 29) + 64
+    bufs = [torch.full((n,), r + 1, dtype=torch.int32, device="cuda") for r in range(2)]
+    try:
+        lb.all_reduce(bufs, "sum")
+    except ddl.DDLError as e:
+        assert e.code == ddl.ERR_TOO_LARGE
+        lb.finalize()
+        return
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    for t in bufs:
+        assert bool((t == 3).all())
+    del bufs
+    lb.finalize()
