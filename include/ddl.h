@@ -164,6 +164,9 @@ ddl_result_t ddl_nvls_attach(ddl_comm_t comm, const void* all_blobs, void* blob_
 ddl_result_t ddl_nvls_bind(ddl_comm_t comm, const void* all_blobs, void* blob_out);
 ddl_result_t ddl_nvls_commit(ddl_comm_t comm, const void* all_blobs);
 ddl_result_t ddl_nvls_buffer(ddl_comm_t comm, void** dev_ptr, size_t* bytes, int* dims_mask);
+/* Self-test of the NVLS setup's descriptor exchange (abstract Unix sockets + SCM_RIGHTS)
+ * inside this process; no GPU.  0 = success. */
+int ddl_debug_nvls_fd_selftest(void);
 
 /* Rank `peer`'s symmetric buffer as mapped into this process (cudaIpc over NVLink; this
  * rank's own buffer for peer == rank).  For measurement and diagnostics (bench.py's

@@ -876,6 +876,41 @@ ddl_result_t ddl_connect(ddl_comm_t c, const void* all_handles) {
 // ------------------------------------------------------------------ NVLS setup rounds
 size_t ddl_nvls_blob_size(void) { return sizeof(nvls::Blob); }
 
+// Self-test of the NVLS descriptor exchange (no GPU): two "ranks" in this process, each with
+// an fd server, send each other two descriptors (a pipe's ends) over the abstract Unix
+// sockets; the received descriptors must refer to the same pipe.  Returns 0 on success.
+int ddl_debug_nvls_fd_selftest(void) {
+  char name[2][64];
+  const int srv[2] = {nvls::fd_server_open(name[0], 0), nvls::fd_server_open(name[1], 1)};
+  if (srv[0] < 0 || srv[1] < 0) return 1;
+  int pfd[2];
+  if (pipe(pfd) != 0) return 2;
+  std::vector<std::vector<int>> got0(2, std::vector<int>(kMaxDims + 1, -1)), got1 = got0;
+  bool ok0 = false, ok1 = false;
+  std::thread t0([&] { ok0 = nvls::fd_recv_all(srv[0], 1, 5000, &got0); });
+  std::thread t1([&] { ok1 = nvls::fd_recv_all(srv[1], 1, 5000, &got1); });
+  const bool s0 = nvls::fd_send(name[1], 0, {0, 3}, {pfd[0], pfd[1]});  // rank 0 -> rank 1
+  const bool s1 = nvls::fd_send(name[0], 1, {0}, {pfd[1]});             // rank 1 -> rank 0
+  t0.join();
+  t1.join();
+  int rc = (ok0 && ok1 && s0 && s1) ? 0 : 3;
+  if (!rc) {  // write through the received write end, read through the received read end
+    const char msg = 'x';
+    char back = 0;
+    if (write(got1[0][3], &msg, 1) != 1 || read(got1[0][0], &back, 1) != 1 || back != 'x') rc = 4;
+    if (!rc && (write(got0[1][0], &msg, 1) != 1 || read(pfd[0], &back, 1) != 1)) rc = 5;
+  }
+  for (auto* g : {&got0, &got1})
+    for (auto& v : *g)
+      for (int fd : v)
+        if (fd >= 0) close(fd);
+  close(pfd[0]);
+  close(pfd[1]);
+  close(srv[0]);
+  close(srv[1]);
+  return rc;
+}
+
 static nvls::Blob* blob_of(const void* all, int r) {
   return reinterpret_cast<nvls::Blob*>(const_cast<char*>(static_cast<const char*>(all)) + (size_t)r * sizeof(nvls::Blob));
 }
@@ -925,29 +960,43 @@ ddl_result_t ddl_nvls_prepare(ddl_comm_t c, size_t bytes, void* out) {
   }
   s.bytes = (bytes + gran - 1) / gran * gran;
   b->bytes = s.bytes;
-  // this rank's NVLS memory: exportable by fabric handle if possible, else by file descriptor
+  // this rank's NVLS memory: exportable by fabric handle if creation AND export work (a
+  // fabric export needs the fabric manager / IMEX service), else by file descriptor.  The
+  // handle type must be the same on every rank: attach checks it.
+  const bool no_fabric = env_size("DDL_NVLS_NO_FABRIC", 0) != 0;
   for (CUmemAllocationHandleType ht : {CU_MEM_HANDLE_TYPE_FABRIC, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR}) {
+    if (ht == CU_MEM_HANDLE_TYPE_FABRIC && no_fabric) continue;
     CUmemAllocationProp ap;
     std::memset(&ap, 0, sizeof(ap));
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = c->device;
     ap.requestedHandleTypes = ht;
-    if (a.memCreate(&s.phys, s.bytes, &ap, 0) == CUDA_SUCCESS) {
+    if (a.memCreate(&s.phys, s.bytes, &ap, 0) != CUDA_SUCCESS) {
+      s.phys = 0;
+      continue;
+    }
+    bool ok;
+    if (ht == CU_MEM_HANDLE_TYPE_FABRIC) {
+      ok = a.memExport(&b->phys_fab, s.phys, ht, 0) == CUDA_SUCCESS;
+    } else {
+      int fd = -1;
+      ok = a.memExport(&fd, s.phys, ht, 0) == CUDA_SUCCESS;
+      s.phys_fd = fd;
+      b->phys_fd = fd;
+    }
+    if (ok) {
       s.htype = ht;
       break;
     }
+    a.memRelease(s.phys);
     s.phys = 0;
   }
   if (!s.phys) { b->status = nvls::kAllocFailed; return DDL_SUCCESS; }
   b->htype = (int32_t)s.htype;
-  if (s.htype == CU_MEM_HANDLE_TYPE_FABRIC) {
-    if (a.memExport(&b->phys_fab, s.phys, s.htype, 0) != CUDA_SUCCESS) { b->status = nvls::kAllocFailed; return DDL_SUCCESS; }
-  } else {
-    int fd = -1;
-    if (a.memExport(&fd, s.phys, s.htype, 0) != CUDA_SUCCESS) { b->status = nvls::kAllocFailed; return DDL_SUCCESS; }
-    s.phys_fd = fd;
-    b->phys_fd = fd;
+  if (s.htype == CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) {  // descriptors travel over a socket
+    s.server = nvls::fd_server_open(b->sock, c->rank);
+    if (s.server < 0) { b->status = nvls::kAllocFailed; return DDL_SUCCESS; }
   }
   // the multicast object of every live dim whose group I lead (c_d = 0)
   for (int li = 0; li < c->topo.nlive; ++li) {
@@ -986,12 +1035,33 @@ ddl_result_t ddl_nvls_attach(ddl_comm_t c, const void* all, void* out) {
       b->status = nvls::kPeerFailed;
       return DDL_SUCCESS;
     }
+  // POSIX fds: every rank sends its memory's descriptor (and those of the multicast objects it
+  // leads) to every peer while a thread receives the peers' -- all inside this round
+  if (s.htype == CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) {
+    s.rx.assign(c->P, std::vector<int>(kMaxDims + 1, -1));
+    bool rx_ok = false;
+    std::thread rx([&] { rx_ok = nvls::fd_recv_all(s.server, c->P - 1, 30000, &s.rx); });
+    std::vector<int> tags{0}, fds{s.phys_fd};
+    for (int li = 0; li < c->topo.nlive; ++li) {
+      const int d = c->topo.live[li];
+      if (s.mc_fd[d] >= 0) {
+        tags.push_back(1 + d);
+        fds.push_back(s.mc_fd[d]);
+      }
+    }
+    bool tx_ok = true;
+    for (int m = 0; m < c->P; ++m)
+      if (m != c->rank) tx_ok = nvls::fd_send(blob_of(all, m)->sock, c->rank, tags, fds) && tx_ok;
+    rx.join();
+    if (!rx_ok || !tx_ok) { b->status = nvls::kImportFailed; return DDL_SUCCESS; }
+  }
+  auto rx_fd = [&](int m, int tag) { return s.rx.empty() ? -1 : s.rx[m][tag]; };
   // unicast mappings: my memory and every peer's
   if (nvls::map_rw(s.phys, s.bytes, 0, c->device, &s.uc[c->rank]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
   for (int m = 0; m < c->P; ++m) {
     if (m == c->rank) continue;
     const nvls::Blob* pb = blob_of(all, m);
-    if (nvls::import_handle(&s.peer_phys[m], s.htype, pb->pid, pb->phys_fd, &pb->phys_fab) != CUDA_SUCCESS) {
+    if (nvls::import_handle(&s.peer_phys[m], s.htype, rx_fd(m, 0), &pb->phys_fab) != CUDA_SUCCESS) {
       s.peer_phys[m] = 0;
       b->status = nvls::kImportFailed;
       return DDL_SUCCESS;
@@ -1004,7 +1074,7 @@ ddl_result_t ddl_nvls_attach(ddl_comm_t c, const void* all, void* out) {
     const int lead = member(c->topo, c->rank, d, 0);
     if (lead != c->rank) {
       const nvls::Blob* lb = blob_of(all, lead);
-      if (nvls::import_handle(&s.mc[d], s.htype, lb->pid, lb->mc_fd[d], &lb->mc_fab[d]) != CUDA_SUCCESS) {
+      if (nvls::import_handle(&s.mc[d], s.htype, rx_fd(lead, 1 + d), &lb->mc_fab[d]) != CUDA_SUCCESS) {
         s.mc[d] = 0;
         b->status = nvls::kImportFailed;
         return DDL_SUCCESS;

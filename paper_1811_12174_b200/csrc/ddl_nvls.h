@@ -14,23 +14,26 @@
 //
 // Driver entry points are resolved at run time (cudaGetDriverEntryPoint), so libddl keeps
 // linking only the static CUDA runtime.  Handle exchange: CU_MEM_HANDLE_TYPE_FABRIC when the
-// allocation supports it (a 64-byte blob), else POSIX file descriptors passed with
-// pidfd_open / pidfd_getfd (same node, same user).
+// allocation and its export support it (a 64-byte blob in the all-gathered round), else POSIX
+// file descriptors, passed between the ranks' processes over abstract-namespace Unix domain
+// sockets with SCM_RIGHTS during the attach round (works without ptrace rights over sibling
+// processes, which pidfd_getfd would need).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <poll.h>
+#include <sys/socket.h>
 #include <sys/syscall.h>
+#include <sys/un.h>
 #include <unistd.h>
 
+#include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <thread>
+#include <vector>
 
-#ifndef SYS_pidfd_open
-#define SYS_pidfd_open 434
-#endif
-#ifndef SYS_pidfd_getfd
-#define SYS_pidfd_getfd 438
-#endif
 
 namespace ddl {
 namespace nvls {
@@ -104,7 +107,109 @@ struct Blob {
   int32_t mc_fd[kMaxDims];
   CUmemFabricHandle phys_fab;
   CUmemFabricHandle mc_fab[kMaxDims];
+  char sock[64];   // abstract Unix socket name of this rank's fd server (POSIX fd exchange)
 };
+
+// ---- file-descriptor exchange over abstract-namespace Unix domain sockets (SCM_RIGHTS)
+// Message: int32 sender, int32 n, int32 tags[n] (tag 0 = the sender's NVLS memory, 1 + d =
+// the multicast object of dim d it leads), with the n descriptors attached.
+inline socklen_t sock_addr(const char* name, sockaddr_un* a) {
+  std::memset(a, 0, sizeof(*a));
+  a->sun_family = AF_UNIX;
+  const size_t len = std::strlen(name);
+  std::memcpy(a->sun_path + 1, name, len);  // leading NUL: abstract namespace
+  return (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + len);
+}
+
+inline int fd_server_open(char* name_out, int rank) {
+  static std::atomic<unsigned> seq{0};
+  std::snprintf(name_out, 63, "ddl-nvls-%d-%d-%u", (int)getpid(), rank, seq.fetch_add(1));
+  const int s = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+  if (s < 0) return -1;
+  sockaddr_un a;
+  const socklen_t len = sock_addr(name_out, &a);
+  if (bind(s, reinterpret_cast<sockaddr*>(&a), len) != 0 || listen(s, 64) != 0) {
+    close(s);
+    return -1;
+  }
+  return s;
+}
+
+inline bool fd_send(const char* peer_name, int sender, const std::vector<int>& tags, const std::vector<int>& fds) {
+  const int s = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+  if (s < 0) return false;
+  sockaddr_un a;
+  const socklen_t len = sock_addr(peer_name, &a);
+  bool ok = false;
+  for (int attempt = 0; attempt < 3000 && !ok; ++attempt) {  // the peer's server exists since prepare
+    ok = connect(s, reinterpret_cast<sockaddr*>(&a), len) == 0;
+    if (!ok) usleep(1000);
+  }
+  if (ok) {
+    int32_t hdr[2 + kMaxDims + 1];
+    const int n = (int)fds.size();
+    hdr[0] = sender;
+    hdr[1] = n;
+    for (int i = 0; i < n; ++i) hdr[2 + i] = tags[i];
+    iovec iov{hdr, (size_t)(2 + n) * sizeof(int32_t)};
+    char ctrl[CMSG_SPACE(sizeof(int) * (kMaxDims + 1))];
+    std::memset(ctrl, 0, sizeof(ctrl));
+    msghdr m;
+    std::memset(&m, 0, sizeof(m));
+    m.msg_iov = &iov;
+    m.msg_iovlen = 1;
+    if (n > 0) {
+      m.msg_control = ctrl;
+      m.msg_controllen = CMSG_SPACE(sizeof(int) * n);
+      cmsghdr* c = CMSG_FIRSTHDR(&m);
+      c->cmsg_level = SOL_SOCKET;
+      c->cmsg_type = SCM_RIGHTS;
+      c->cmsg_len = CMSG_LEN(sizeof(int) * n);
+      std::memcpy(CMSG_DATA(c), fds.data(), sizeof(int) * n);
+    }
+    ok = sendmsg(s, &m, 0) == (ssize_t)iov.iov_len;
+  }
+  close(s);
+  return ok;
+}
+
+// Accept `expect` messages (timeout_ms overall); got[sender][tag] = received descriptor.
+inline bool fd_recv_all(int server, int expect, int timeout_ms, std::vector<std::vector<int>>* got) {
+  int done = 0;
+  while (done < expect) {
+    pollfd pf{server, POLLIN, 0};
+    if (poll(&pf, 1, timeout_ms) <= 0) return false;
+    const int c = accept4(server, nullptr, nullptr, SOCK_CLOEXEC);
+    if (c < 0) return false;
+    int32_t hdr[2 + kMaxDims + 1];
+    iovec iov{hdr, sizeof(hdr)};
+    char ctrl[CMSG_SPACE(sizeof(int) * (kMaxDims + 1))];
+    msghdr m;
+    std::memset(&m, 0, sizeof(m));
+    m.msg_iov = &iov;
+    m.msg_iovlen = 1;
+    m.msg_control = ctrl;
+    m.msg_controllen = sizeof(ctrl);
+    const ssize_t r = recvmsg(c, &m, 0);
+    close(c);
+    if (r < (ssize_t)(2 * sizeof(int32_t))) return false;
+    const int sender = hdr[0], n = hdr[1];
+    if (sender < 0 || sender >= (int)got->size() || n < 0 || n > kMaxDims + 1) return false;
+    int fds[kMaxDims + 1];
+    cmsghdr* cm = CMSG_FIRSTHDR(&m);
+    if (n > 0) {
+      if (!cm || cm->cmsg_type != SCM_RIGHTS) return false;
+      std::memcpy(fds, CMSG_DATA(cm), sizeof(int) * n);
+    }
+    for (int i = 0; i < n; ++i) {
+      const int tag = hdr[2 + i];
+      if (tag < 0 || tag > kMaxDims) return false;
+      (*got)[sender][tag] = fds[i];
+    }
+    ++done;
+  }
+  return true;
+}
 
 // Per-communicator state.
 struct State {
@@ -122,24 +227,20 @@ struct State {
   bool mc_bound[kMaxDims] = {};
   char* mcva[kMaxDims] = {};
   int mask = 0;  // dims running in the switch (after commit)
+  int server = -1;                                 // fd server socket (POSIX fd exchange)
+  std::vector<std::vector<int>> rx;                // [sender][tag] descriptors received
   State() {
     for (int d = 0; d < kMaxDims; ++d) mc_fd[d] = -1;
   }
 };
 
-// Import a peer's shareable handle: fabric blob, or (pid, fd) through pidfd_getfd.
-inline CUresult import_handle(CUmemGenericAllocationHandle* h, CUmemAllocationHandleType ht, int pid, int fd,
+// Import a peer's shareable handle: its fabric blob, or the descriptor it sent us.
+inline CUresult import_handle(CUmemGenericAllocationHandle* h, CUmemAllocationHandleType ht, int local_fd,
                               const CUmemFabricHandle* fab) {
   Api& a = api();
   if (ht == CU_MEM_HANDLE_TYPE_FABRIC) return a.memImport(h, const_cast<CUmemFabricHandle*>(fab), ht);
-  const int pfd = (int)syscall(SYS_pidfd_open, pid, 0);
-  if (pfd < 0) return CUDA_ERROR_INVALID_HANDLE;
-  const int local = (int)syscall(SYS_pidfd_getfd, pfd, fd, 0);
-  close(pfd);
-  if (local < 0) return CUDA_ERROR_INVALID_HANDLE;
-  CUresult r = a.memImport(h, reinterpret_cast<void*>((uintptr_t)local), ht);
-  close(local);
-  return r;
+  if (local_fd < 0) return CUDA_ERROR_INVALID_HANDLE;
+  return a.memImport(h, reinterpret_cast<void*>((uintptr_t)local_fd), ht);
 }
 
 inline CUresult map_rw(CUmemGenericAllocationHandle h, size_t bytes, size_t align, int dev, char** va) {
@@ -197,6 +298,15 @@ inline void teardown(State& s, const Topo& t, int rank) {
   s.phys = 0;
   if (s.phys_fd >= 0) close(s.phys_fd);
   s.phys_fd = -1;
+  if (s.server >= 0) close(s.server);
+  s.server = -1;
+  for (auto& v : s.rx)
+    for (int& fd : v)
+      if (fd >= 0) {
+        close(fd);
+        fd = -1;
+      }
+  s.rx.clear();
   s.mask = 0;
   s.stage = 0;
 }

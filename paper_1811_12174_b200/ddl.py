@@ -69,6 +69,7 @@ def _load() -> ctypes.CDLL:
         "ddl_buffer": (c_int, [c_void, pp, ctypes.POINTER(c_size)]),
         "ddl_peer_buffer": (c_int, [c_void, c_int, pp, ctypes.POINTER(c_size)]),
         "ddl_nvls_blob_size": (c_size, []),
+        "ddl_debug_nvls_fd_selftest": (c_int, []),
         "ddl_nvls_prepare": (c_int, [c_void, c_size, c_void]),
         "ddl_nvls_attach": (c_int, [c_void, c_void, c_void]),
         "ddl_nvls_bind": (c_int, [c_void, c_void, c_void]),

@@ -228,3 +228,10 @@ def test_auto_dims():
     assert ddl.auto_dims(16, 8) == [8, 2]
     with pytest.raises(ddl.DDLError):
         ddl.auto_dims(8, 3)
+
+
+def test_nvls_descriptor_exchange_selftest():
+    """The NVLS setup passes POSIX file descriptors between rank processes over abstract Unix
+    sockets (SCM_RIGHTS); the library's self-test exchanges a pipe's ends between two
+    in-process "ranks" and checks that the received descriptors are the same pipe."""
+    assert ddl.lib().ddl_debug_nvls_fd_selftest() == 0
