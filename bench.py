@@ -46,13 +46,29 @@ DIMS_FOR_N = {1: "2x4", 2: "2", 4: "2x2", 8: "2x4"}
 TRAFFIC_KEY = "resnet50-grad-set 8 virtual ranks dims 2x4 avg, grouped"
 
 
+def source_hash() -> str:
+    """sha256 of the DEVICE sources libddl.so's kernels are compiled from (the .cuh kernel
+    files, the shared planner header, build.sh's flags): ties a committed ncu capture of a
+    kernel's DRAM traffic to the kernel code it measured."""
+    import hashlib
+    h = hashlib.sha256()
+    src = os.path.join(ROOT, "paper_1811_12174_b200", "csrc")
+    for name in sorted(f for f in os.listdir(src) if f.endswith(".cuh")) + ["ddl_plan.h", "../../build.sh"]:
+        with open(os.path.join(src, name), "rb") as f:
+            h.update(name.encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
 def profiled_traffic(workload_key: str):
     """DRAM bytes per step of the timed kernels from the committed ncu capture
-    (profiles/traffic.json, written from an `ncu --set full` run of scripts/profile_step.py)."""
+    (profiles/traffic.json, written from an `ncu --set full` run of scripts/profile_step.py),
+    only if that capture measured THIS build (source hash) and workload -- else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             d = json.load(f)
-        return d["dram_bytes_per_step"] if d.get("workload") == workload_key else None
+        if d.get("workload") != workload_key or d.get("source_hash") != source_hash():
+            return None
+        return d["dram_bytes_per_step"]
     except Exception:
         return None
 
@@ -404,7 +420,8 @@ def run_loopback(args):
                      "frac": achieved / hbm_peak,
                      "traffic": (tr // launches_per_step if (tr := profiled_traffic(TRAFFIC_KEY))
                                  and dims == [4, 2] else None),
-                     "traffic_unit": "DRAM bytes per launch, ncu --set full of one bench step, profiles/traffic.json",
+                     "traffic_unit": "DRAM bytes per launch, ncu --set full of one bench step, profiles/traffic.json "
+                                     "(null unless that capture measured this build: source hash)",
                      "algorithmic_bytes_per_launch": algo_bytes // args.steps // launches_per_step,
                      "peak_source": peak_src,
                      "kernel": "ddl_multi_kernel<float> (grouped: 5 buckets x 8 virtual ranks in one launch, "

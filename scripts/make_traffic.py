@@ -1,7 +1,10 @@
 """Write profiles/traffic.json (read by bench.py for roofline.traffic) from an `ncu --set
-full` capture of scripts/profile_step.py (5 ddl_hier_kernel launches = one bench step):
-  python scripts/make_traffic.py gpurun_out/r01_v6_step.ncu-rep profiles/r01_v6_step_details.csv"""
+full` capture of scripts/profile_step.py (one grouped launch = one bench step):
+  python scripts/make_traffic.py gpurun_out/r02_v1_step.ncu-rep profiles/r02_v1_step_details.csv [srchash file]
+The source hash of the captured build is taken from the capture's <tag>_srchash.txt
+(written on the GPU box by scripts/round_capture.sh) when given, else from this tree."""
 import csv, io, json, os, subprocess, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 rep, details = sys.argv[1], sys.argv[2]
 metrics = "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct," \
@@ -28,6 +31,7 @@ out = {"source": f"ncu --set full --clock-control none, {details} ({len(launches
        "dram_bytes_per_step": sum(l["dram_bytes"] for l in launches),
        "ncu_kernel_us_per_step": round(sum(l["us"] for l in launches), 3),
        "workload": "resnet50-grad-set 8 virtual ranks dims 2x4 avg, grouped",
+       "source_hash": (open(sys.argv[3]).read().strip() if len(sys.argv) > 3 else __import__("bench").source_hash()),
        "launches": launches}
 with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json"), "w") as f:
     json.dump(out, f, indent=1)

@@ -1,6 +1,7 @@
 set -x
 TAG=${TAG:-r02_v1}
 mkdir -p gpurun_out
+python -c "import bench; print(bench.source_hash())" > gpurun_out/${TAG}_srchash.txt
 timeout 1500 python -m pytest tests -m gpu -q --timeout 600 2>&1 | tail -4 > gpurun_out/${TAG}_pytest_gpu.txt
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.txt 2>&1
 timeout 300 python bench.py 2>&1 | tail -1 > gpurun_out/${TAG}_bench.json
