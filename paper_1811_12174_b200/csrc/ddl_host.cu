@@ -942,7 +942,8 @@ ddl_result_t ddl_nvls_prepare(ddl_comm_t c, size_t bytes, void* out) {
   nvls::Api& a = nvls::api();
   if (!a.ok || c->P < 2) { b->status = nvls::kNoApi; return DDL_SUCCESS; }
   int mcs = 0;
-  if (a.getAttr(&mcs, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, c->device) != CUDA_SUCCESS || !mcs) {
+  if (a.deviceGet(&s.cudev, c->device) != CUDA_SUCCESS ||
+      a.getAttr(&mcs, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, s.cudev) != CUDA_SUCCESS || !mcs) {
     b->status = nvls::kNoMulticast;
     return DDL_SUCCESS;
   }
@@ -958,6 +959,16 @@ ddl_result_t ddl_nvls_prepare(ddl_comm_t c, size_t bytes, void* out) {
     // the minimum granularity (2 MiB here): the recommended one is 512 MiB per rank
     if (a.mcGranularity(&g, &mp, CU_MULTICAST_GRANULARITY_MINIMUM) == CUDA_SUCCESS && g > gran) gran = g;
   }
+  {  // and the physical allocation's granularity
+    CUmemAllocationProp ap;
+    std::memset(&ap, 0, sizeof(ap));
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = c->device;
+    size_t g = 0;
+    if (a.memGranularity(&g, &ap, CU_MEM_ALLOC_GRANULARITY_MINIMUM) == CUDA_SUCCESS && g > gran) gran = g;
+  }
+  s.gran = gran;
   s.bytes = (bytes + gran - 1) / gran * gran;
   b->bytes = s.bytes;
   // this rank's NVLS memory: exportable by fabric handle if creation AND export work (a
@@ -1057,7 +1068,7 @@ ddl_result_t ddl_nvls_attach(ddl_comm_t c, const void* all, void* out) {
   }
   auto rx_fd = [&](int m, int tag) { return s.rx.empty() ? -1 : s.rx[m][tag]; };
   // unicast mappings: my memory and every peer's
-  if (nvls::map_rw(s.phys, s.bytes, 0, c->device, &s.uc[c->rank]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
+  if (nvls::map_rw(s.phys, s.bytes, s.gran, c->device, &s.uc[c->rank]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
   for (int m = 0; m < c->P; ++m) {
     if (m == c->rank) continue;
     const nvls::Blob* pb = blob_of(all, m);
@@ -1066,7 +1077,7 @@ ddl_result_t ddl_nvls_attach(ddl_comm_t c, const void* all, void* out) {
       b->status = nvls::kImportFailed;
       return DDL_SUCCESS;
     }
-    if (nvls::map_rw(s.peer_phys[m], s.bytes, 0, c->device, &s.uc[m]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
+    if (nvls::map_rw(s.peer_phys[m], s.bytes, s.gran, c->device, &s.uc[m]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
   }
   // join every live dim's group multicast object
   for (int li = 0; li < c->topo.nlive; ++li) {
@@ -1080,7 +1091,7 @@ ddl_result_t ddl_nvls_attach(ddl_comm_t c, const void* all, void* out) {
         return DDL_SUCCESS;
       }
     }
-    if (a.mcAddDevice(s.mc[d], c->device) != CUDA_SUCCESS) { b->status = nvls::kAddFailed; return DDL_SUCCESS; }
+    if (a.mcAddDevice(s.mc[d], s.cudev) != CUDA_SUCCESS) { b->status = nvls::kAddFailed; return DDL_SUCCESS; }
     s.mc_added[d] = true;
   }
   s.stage = 2;
@@ -1100,7 +1111,7 @@ ddl_result_t ddl_nvls_bind(ddl_comm_t c, const void* all, void* out) {
     const int d = c->topo.live[li];
     if (a.mcBindMem(s.mc[d], 0, s.phys, 0, s.bytes, 0) != CUDA_SUCCESS) { b->status = nvls::kBindFailed; return DDL_SUCCESS; }
     s.mc_bound[d] = true;
-    if (nvls::map_rw(s.mc[d], s.bytes, 0, c->device, &s.mcva[d]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
+    if (nvls::map_rw(s.mc[d], s.bytes, s.gran, c->device, &s.mcva[d]) != CUDA_SUCCESS) { b->status = nvls::kMapFailed; return DDL_SUCCESS; }
   }
   s.stage = 3;
   b->status = nvls::kOk;

@@ -41,6 +41,7 @@ namespace nvls {
 struct Api {
   bool ok = false;
   CUresult (*getAttr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+  CUresult (*deviceGet)(CUdevice*, int) = nullptr;
   CUresult (*mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
   CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
   CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
@@ -77,7 +78,8 @@ inline bool resolve(const char* name, F* fn) {
 inline Api& api() {
   static Api a = [] {
     Api x;
-    x.ok = resolve("cuDeviceGetAttribute", &x.getAttr) && resolve("cuMulticastCreate", &x.mcCreate) &&
+    x.ok = resolve("cuDeviceGetAttribute", &x.getAttr) && resolve("cuDeviceGet", &x.deviceGet) &&
+           resolve("cuMulticastCreate", &x.mcCreate) &&
            resolve("cuMulticastAddDevice", &x.mcAddDevice) && resolve("cuMulticastBindMem", &x.mcBindMem) &&
            resolve("cuMulticastUnbind", &x.mcUnbind) && resolve("cuMulticastGetGranularity", &x.mcGranularity) &&
            resolve("cuMemCreate", &x.memCreate) && resolve("cuMemGetAllocationGranularity", &x.memGranularity) &&
@@ -214,7 +216,9 @@ inline bool fd_recv_all(int server, int expect, int timeout_ms, std::vector<std:
 // Per-communicator state.
 struct State {
   int stage = 0;  // 0 none, 1 prepared, 2 attached, 3 bound, 4 ready
-  int dev = 0;
+  int dev = 0;          // runtime ordinal (access descriptors take it)
+  CUdevice cudev = 0;   // driver handle of that device (multicast calls)
+  size_t gran = 0;      // multicast / allocation granularity: VA alignment
   CUmemAllocationHandleType htype = CU_MEM_HANDLE_TYPE_NONE;
   size_t bytes = 0;
   CUmemGenericAllocationHandle phys = 0;
@@ -281,7 +285,7 @@ inline void teardown(State& s, const Topo& t, int rank) {
   if (!api().ok) return;
   for (int d = 0; d < kMaxDims; ++d) {
     unmap(&s.mcva[d], s.bytes);
-    if (s.mc_bound[d]) api().mcUnbind(s.mc[d], s.dev, 0, s.bytes);
+    if (s.mc_bound[d]) api().mcUnbind(s.mc[d], s.cudev, 0, s.bytes);
     s.mc_bound[d] = false;
     if (s.mc[d]) api().memRelease(s.mc[d]);
     s.mc[d] = 0;
