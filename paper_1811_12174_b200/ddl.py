@@ -471,13 +471,14 @@ def auto_dims(world: int, local_world: int | None = None) -> list[int]:
     return [local_world] if nodes == 1 else [local_world, nodes]
 
 
-def init(dims=None, group=None, max_bytes: int = 256 << 20) -> Comm:
+def init(dims=None, group=None, max_bytes: int = 256 << 20, nvls_bytes: int | None = None) -> Comm:
     """``ddl.init(dims)``: the analogue of the paper's ``import ddl`` + ``ddlrun`` setup
      under torchrun.  ``dims="auto"`` picks :func:`auto_dims`.  The
     environment variable ``DDL_DIMS`` (e.g. ``2x4``, or ``auto``) overrides ``dims`` -- the
-    role of ddlrun's topology configuration -- and must be equal on every rank."""
+    role of ddlrun's topology configuration -- and must be equal on every rank.
+    ``nvls_bytes`` (or DDL_NVLS_BYTES) requests the NVSwitch multicast phases (Comm)."""
     import torch.distributed as dist
-    return Comm(resolve_dims(dims, dist.get_world_size(group)), group, max_bytes)
+    return Comm(resolve_dims(dims, dist.get_world_size(group)), group, max_bytes, nvls_bytes=nvls_bytes)
 
 
 def resolve_dims(dims, world: int, local_world: int | None = None) -> list[int]:
