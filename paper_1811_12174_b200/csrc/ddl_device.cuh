@@ -1106,7 +1106,6 @@ struct MParams {
   int bk0[kMaxChannels + 1];   // and runs buckets order[bk0[ch] .. bk0[ch+1]) in that order
   int order[kMaxBuckets];
   int maxk;                    // most bucket-waves in one channel
-  int lookahead;               // 1: item k+1's first RS phase before item k's last AG barrier
 };
 
 template <typename T>
@@ -1140,29 +1139,16 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
   };
   const int cc = mp.cta0[ch + 1] - mp.cta0[ch];
   const int nk = mp.bk0[ch + 1] - mp.bk0[ch];
-  // the channel's items: (bucket, wave) in execution order; item k releases epoch e + k
-  __shared__ uint8_t s_ib[kMaxBuckets * 32], s_iw[kMaxBuckets * 32];
-  __shared__ int s_ni;
-  if (threadIdx.x == 0) {
-    int ni = 0;
-    for (int kw = 0; kw < nk; ++kw) {
-      const int b = mp.order[mp.bk0[ch] + kw];
-      const int nw = mp.b[b].nwaves > 1 ? mp.b[b].nwaves : 1;
-      for (int w = 0; w < nw && ni < kMaxBuckets * 32; ++w, ++ni) {
-        s_ib[ni] = (uint8_t)b;
-        s_iw[ni] = (uint8_t)w;
-      }
-    }
-    s_ni = ni;
-  }
-  __syncthreads();
-  const int ni = s_ni;
   uint32_t ew = e;
-  int cur = -1;
-  auto load = [&](int k) {  // point sp at item k's bucket
-    if (k == cur) return;
-    const MBucket& B = mp.b[s_ib[k]];
-    __syncthreads();  // the previous item's readers of sp are done
+  int seq = 0;  // bucket-waves done by this channel
+#pragma unroll 1
+  for (int kw = 0; kw < nk; ++kw) {
+    const MBucket& B = mp.b[mp.order[mp.bk0[ch] + kw]];
+#pragma unroll 1
+    for (int w = 0; w < (B.nwaves > 1 ? B.nwaves : 1); ++w, ++seq) {
+    const int k = seq;
+    ew = e + (uint32_t)k;
+    __syncthreads();  // the previous bucket's readers of sp are done
     if (threadIdx.x == 0) {
       sp.n = B.n;
       sp.q = B.q;
@@ -1174,49 +1160,28 @@ __global__ void __launch_bounds__(kThreads, DDL_TMA_MINBLOCKS) ddl_multi_kernel(
       sp.out[threadIdx.x] = B.buf[threadIdx.x];
     }
     __syncthreads();
-    cur = k;
-  };
-  // RS phase j / AG phase jj of item k, each after its barrier (the first RS phase of item
-  // k > 0, and of every item in loopback, has none: inputs are ready at launch / barrier 0
-  // of item 0, and no item writes what another reads)
-  auto rs = [&](int k, int j) -> bool {
-    load(k);
-    const uint32_t ek = e + (uint32_t)k;
-    if (!(j == 0 && (k > 0 || p0.loopback)) && !dbarrier(sp, me, j, barrier_npeers(t, j), ek, group_peer(j)))
-      return false;
-    tev(k, j, 0);
-    PhaseCtx x = phase_ctx(sp, me, kPhRS, t.live[j], j == 0, j == L - 1);
-    x.s = s_iw[k] * cc + lc;
-    tma_phase<T>(sp, me, x, pp);
-    tev(k, j, 1);
-    return true;
-  };
-  auto ag = [&](int k, int jj) -> bool {
-    load(k);
-    const int j = L + jj;
-    if (!dbarrier(sp, me, j, barrier_npeers(t, j), e + (uint32_t)k, group_peer(j))) return false;
-    tev(k, j, 0);
-    PhaseCtx x = phase_ctx(sp, me, kPhAG, t.live[L - 1 - jj], false, jj == L - 1);
-    x.s = s_iw[k] * cc + lc;
-    tma_phase<T>(sp, me, x, pp);
-    tev(k, j, 1);
-    return true;
-  };
-  // Lookahead (mp.lookahead): item k+1's first RS phase -- no barrier, DRAM-heavy -- runs
-  // before item k's last allgather barrier, so the time a CTA would spend waiting there for
-  // slower chain members goes into useful streaming; the results are unchanged.
-#pragma unroll 1
-  for (int k = 0; k < ni; ++k) {
-    ew = e + (uint32_t)k;
-    if (!(mp.lookahead && k > 0) && L > 0 && !rs(k, 0)) return;
-    for (int j = 1; j < L; ++j)
-      if (!rs(k, j)) return;
-    for (int jj = 0; jj + 1 < L; ++jj)
-      if (!ag(k, jj)) return;
-    if (mp.lookahead && k + 1 < ni && !rs(k + 1, 0)) return;
-    if (L > 0 && !ag(k, L - 1)) return;
+    const KParams& p = sp;
+    for (int j = 0; j < L; ++j) {
+      if (!(j == 0 && (k > 0 || p0.loopback)) && !dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j)))
+        return;
+      tev(k, j, 0);
+      PhaseCtx x = phase_ctx(p, me, kPhRS, t.live[j], j == 0, j == L - 1);
+      x.s = w * cc + lc;
+      tma_phase<T>(p, me, x, pp);
+      tev(k, j, 1);
+    }
+    for (int jj = 0; jj < L; ++jj) {
+      const int j = L + jj;
+      if (!dbarrier(p, me, j, barrier_npeers(t, j), ew, group_peer(j))) return;
+      tev(k, j, 0);
+      PhaseCtx x = phase_ctx(p, me, kPhAG, t.live[L - 1 - jj], false, jj == L - 1);
+      x.s = w * cc + lc;
+      tma_phase<T>(p, me, x, pp);
+      tev(k, j, 1);
+    }
+    }
   }
-  if (ni > 0 && L > 0 && !p0.loopback && !dbarrier(sp, me, 2 * L, barrier_npeers(t, 2 * L), ew, group_peer(2 * L)))
+  if (nk > 0 && L > 0 && !p0.loopback && !dbarrier(sp, me, 2 * L, barrier_npeers(t, 2 * L), ew, group_peer(2 * L)))
     return;
   rank_epoch_end(p0, me, e + (uint32_t)(mp.maxk > 0 ? mp.maxk - 1 : 0), 0);
 }

@@ -157,7 +157,6 @@ struct ddl_comm {
   int group_waves = 1;                     // DDL_GROUP_WAVES: waves per bucket in a grouped all-reduce (0 = auto)
   size_t group_wave_bytes = 0;             // DDL_GROUP_WAVE_MB: per-wave partial footprint budget (0 = off)
   int group_order = 0;                     // DDL_GROUP_ORDER: 0 LPT (longest first), 1 ascending within a channel
-  int group_lookahead = 0;                 // DDL_GROUP_LOOKAHEAD: next item's first RS phase before the last AG barrier
   int waves = 0;                           // DDL_WAVES: slices per CTA per hierarchical call (0 = auto)
   size_t wave_slice_bytes = 112 << 10;     // auto: target per-CTA slice of one wave
   size_t min_wave_slice_bytes = 16 << 10;  // no waves below this slice size
@@ -273,7 +272,6 @@ void apply_env(ddl_comm* c) {
   c->group_waves = (int)env_size("DDL_GROUP_WAVES", c->group_waves);
   c->group_wave_bytes = env_size("DDL_GROUP_WAVE_MB", c->group_wave_bytes >> 20) << 20;
   c->group_order = (int)env_size("DDL_GROUP_ORDER", c->group_order);
-  c->group_lookahead = (int)env_size("DDL_GROUP_LOOKAHEAD", c->group_lookahead);
   c->nvls_dims_mask = std::getenv("DDL_NVLS_DIMS") ? (int)env_size("DDL_NVLS_DIMS", 0) : -1;
   c->nvls_emulate = env_size("DDL_NVLS_EMULATE", 0) != 0;
   c->l2hint = (int)env_size("DDL_L2_HINTS", c->l2hint);
@@ -1608,7 +1606,6 @@ static ddl_result_t launch_multi(const ddl_comm* c, const uint64_t* ns, void* co
       ++used;
     }
     mp.nchan = K;
-    mp.lookahead = c->group_lookahead ? 1 : 0;
     int pos = 0, maxk = 0;
     for (int ch = 0; ch <= kMaxChannels; ++ch) {
       mp.cta0[ch] = ch == 0 ? 0 : mp.cta0[ch - 1] + (ch - 1 < K ? cc[ch - 1] : 0);
