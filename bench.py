@@ -481,18 +481,16 @@ def peer_copy_gbs(comm, P, rank, nbytes, offset, reps=10):
     receives one stream: GB/s per direction per GPU, max time over ranks."""
     import torch
     import torch.distributed as dist
-    n = nbytes // 4
-    src = comm.buffer(n, torch.float32, offset)
-    dst = comm.peer_buffer((rank + 1) % P, n, torch.float32, offset + (nbytes + 255) // 256 * 256)
+    peer, dst_off = (rank + 1) % P, offset + (nbytes + 255) // 256 * 256
     stream = torch.cuda.current_stream()
     for _ in range(2):
-        dst.copy_(src)
+        comm.peer_copy(peer, offset, dst_off, nbytes, stream)
     torch.cuda.synchronize()
     dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(reps):
-        dst.copy_(src)
+        comm.peer_copy(peer, offset, dst_off, nbytes, stream)
     b.record(stream)
     torch.cuda.synchronize()
     t = torch.tensor([a.elapsed_time(b) / reps], device="cuda" if dist.get_backend() == "nccl" else "cpu")

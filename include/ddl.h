@@ -173,6 +173,12 @@ int ddl_debug_nvls_fd_selftest(void);
  * peer-copy peak); writing into it races with the peer's collectives unless the caller
  * orders them.  DDL_ERR_NOT_CONNECTED before ddl_connect. */
 ddl_result_t ddl_peer_buffer(ddl_comm_t comm, int peer, void** dev_ptr, size_t* bytes);
+/* Enqueue one copy of `bytes` from this rank's symmetric buffer (+src_offset) into rank
+ * `peer`'s (+dst_offset) over the cudaIpc mapping (cudaMemcpyAsync: the copy engines) --
+ * the peer-copy reference bench.py measures beside the NVLink roofline.  Same caveat as
+ * ddl_peer_buffer: the caller orders it against the peer's collectives. */
+ddl_result_t ddl_peer_copy(ddl_comm_t comm, int peer, size_t src_offset, size_t dst_offset, size_t bytes,
+                           void* stream);
 
 /* Registered buffers (SURVEY 8(b) ddl_register): persistent user buffers -- e.g. DDP's
  * gradient buckets -- made zero-copy.  Collective: every rank calls

@@ -1152,6 +1152,16 @@ ddl_result_t ddl_peer_buffer(ddl_comm_t c, int peer, void** dev_ptr, size_t* byt
   return DDL_SUCCESS;
 }
 
+ddl_result_t ddl_peer_copy(ddl_comm_t c, int peer, size_t src_offset, size_t dst_offset, size_t bytes, void* stream) {
+  if (!c || c->loopback || peer < 0 || peer >= c->P) return DDL_ERR_INVALID_ARGUMENT;
+  if (src_offset + bytes > c->max_bytes || dst_offset + bytes > c->max_bytes) return DDL_ERR_TOO_LARGE;
+  if (peer != c->rank && !c->peer_mapped[peer]) return DDL_ERR_NOT_CONNECTED;
+  DDL_ON_DEVICE(c->device);
+  DDL_CUDA(cudaMemcpyAsync(c->sym_of(peer) + dst_offset, c->sym_of(c->rank) + src_offset, bytes,
+                           cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return DDL_SUCCESS;
+}
+
 ddl_result_t ddl_buffer(ddl_comm_t c, void** dev_ptr, size_t* bytes) {
   if (!c || !dev_ptr || !bytes || c->loopback) return DDL_ERR_INVALID_ARGUMENT;
   *dev_ptr = c->alloc + c->flags_bytes;

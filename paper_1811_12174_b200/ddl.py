@@ -68,6 +68,7 @@ def _load() -> ctypes.CDLL:
         "ddl_connect": (c_int, [c_void, c_void]),
         "ddl_buffer": (c_int, [c_void, pp, ctypes.POINTER(c_size)]),
         "ddl_peer_buffer": (c_int, [c_void, c_int, pp, ctypes.POINTER(c_size)]),
+        "ddl_peer_copy": (c_int, [c_void, c_int, c_size, c_size, c_size, c_void]),
         "ddl_nvls_blob_size": (c_size, []),
         "ddl_debug_nvls_fd_selftest": (c_int, []),
         "ddl_nvls_prepare": (c_int, [c_void, c_size, c_void]),
@@ -331,18 +332,13 @@ class Comm:
         full = _tensor_from_ptr(self.buffer_ptr, self.buffer_bytes, self.device)
         return full[offset_bytes:offset_bytes + count * esz].view(dtype)
 
-    def peer_buffer(self, peer: int, count: int, dtype, offset_bytes: int = 0):
-        """A tensor view of rank ``peer``'s symmetric buffer as mapped here (over NVLink);
-        for measurement only (bench.py's peer-copy peak)."""
-        torch = _torch()
-        p = ctypes.c_void_p()
-        n = ctypes.c_size_t()
-        _check(_lib.ddl_peer_buffer(self.h, peer, ctypes.byref(p), ctypes.byref(n)), "ddl_peer_buffer")
-        esz = torch.tensor([], dtype=dtype).element_size()
-        if offset_bytes + count * esz > n.value:
-            raise DDLError(ERR_TOO_LARGE, "view outside the peer's symmetric buffer")
-        full = _tensor_from_ptr(p.value, n.value, self.device)
-        return full[offset_bytes:offset_bytes + count * esz].view(dtype)
+    def peer_copy(self, peer: int, src_offset: int, dst_offset: int, nbytes: int, stream=None) -> None:
+        """Enqueue a copy of nbytes from this rank's symmetric buffer into rank ``peer``'s over
+        the cudaIpc mapping (copy engines); for measurement only (bench.py's peer-copy peak).
+        Raw pointers stay inside the library: a torch view of peer memory would be attributed
+        to the peer's device."""
+        _check(_lib.ddl_peer_copy(self.h, peer, src_offset, dst_offset, nbytes, _stream(stream, self.device)),
+               "ddl_peer_copy")
 
     def _zero_copy(self, ptr: int, nbytes: int) -> bool:
         """Inside the symmetric buffer or the NVLS buffer (read by peers in place)."""
