@@ -75,6 +75,34 @@ def run_group(force):
 
 run_group(TMA)
 run_group(WAVES)
+# round 2: the LL kernel in loopback (forced), the NVLS kernel (PATH 7) with its data flow
+# emulated (every dim in the "switch", and a mixed per-dim mask), g_d = 1 dims
+lb = ddl.Loopback(4, [2, 2])
+lb.set_algo(ddl.ALGO_LL, 0)
+for n in (3, 2049):
+    for dt in (torch.float32, torch.bfloat16, torch.int32):
+        bufs = [torch.full((n,), r + 1, dtype=dt, device="cuda") for r in range(4)]
+        lb.all_reduce(bufs)
+        check(bufs, 10)
+lb.finalize()
+for force in ({"DDL_NVLS_EMULATE": "1"}, {"DDL_NVLS_EMULATE": "1", "DDL_NVLS_DIMS": "2"}):
+    os.environ.update(force)
+    lb = ddl.Loopback(8, [2, 2, 2])
+    for k in force:
+        os.environ.pop(k, None)
+    lb.set_algo(ddl.ALGO_HIER, 0)
+    for n in (8, 70_000):
+        for dt in (torch.float32, torch.int32):
+            bufs = [torch.full((n,), r + 1, dtype=dt, device="cuda") for r in range(8)]
+            lb.all_reduce(bufs)
+            check(bufs, 36)
+    lb.finalize()
+lb = ddl.Loopback(8, [4, 1, 2])
+lb.set_algo(ddl.ALGO_HIER, 0)
+bufs = [torch.full((1003,), r + 1.0, device="cuda") for r in range(8)]
+lb.all_reduce(bufs)
+check(bufs, 36)
+lb.finalize()
 for n in (1001, (32 << 20) // 4 + 3):   # register path, then the TMA-ring path (>= 32 MiB)
     ins = [torch.full((n,), float(j), device="cuda") for j in range(3)]
     out = torch.empty(n, device="cuda")
