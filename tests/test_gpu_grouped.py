@@ -241,3 +241,27 @@ def test_reduce_scatter_workspace_growth_refused_in_capture():
     for r in range(P):
         assert same_bits(to_host(outs[r]), want[r]), r
     lb.finalize()
+
+
+def test_grouped_randomized_instances():
+    """Randomized grouped all-reduces (SPEC S:L609 style): random P <= 16, factorisation (g_d = 1
+    dims included), dtype, op, 1-8 buckets of random (incl. empty / one-shot-sized / ragged)
+    lengths, 1-4 channels, 1-3 waves per bucket; every bucket bit-exact vs the oracle."""
+    rng = np.random.Generator(np.random.PCG64(4242))
+    cases = [(2, [2]), (3, [3]), (4, [2, 2]), (4, [4, 1]), (6, [3, 2]), (8, [4, 2]), (8, [2, 2, 2]), (8, [1, 8]),
+             (12, [3, 4]), (16, [4, 4]), (16, [2, 8])]
+    for inst in range(24):
+        P, dims = cases[int(rng.integers(len(cases)))]
+        dtype = ["int32", "float32", "bfloat16"][int(rng.integers(3))]
+        op = "sum" if dtype == "int32" else ["sum", "avg"][int(rng.integers(2))]
+        nbk = int(rng.integers(1, 9))
+        sizes = [int(rng.choice([0, 1, 17, 5000, 70_001, 300_000, 999_983])) for _ in range(nbk)]
+        env = {"DDL_CHANNELS": str(int(rng.integers(1, 5))), "DDL_GROUP_WAVES": str(int(rng.integers(1, 4))),
+               "DDL_MIN_WAVE_SLICE_BYTES": "0"}
+        lb = with_env(env, lambda: ddl.Loopback(P, dims))
+        hosts, devs = make(P, dtype, sizes, seed=9000 + 10 * inst)
+        lb.all_reduce_many(devs, op)
+        torch.cuda.synchronize()
+        assert lb.async_error() == ddl.SUCCESS, inst
+        check_buckets(devs, hosts, dims, dtype, op, f"inst {inst} P={P} dims={dims} {env} sizes={sizes}")
+        lb.finalize()

@@ -118,3 +118,29 @@ def test_nvls_emulated_two_member_phases_bit_exact():
         for r in range(8):
             assert same_bits(to_host(dev[r]), want[r]), (dtype, r)
     lb.finalize()
+
+
+def test_nvls_emulated_randomized():
+    """Random P, factorisation, per-dim NVLS mask, dtype, op and length (16-B multiples and
+    ragged, which keep the direct path): int32 exact, fp32 / bf16 within the any-order bound,
+    replicas identical."""
+    rng = np.random.Generator(np.random.PCG64(77))
+    cases = [(2, [2]), (4, [2, 2]), (6, [3, 2]), (8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (16, [4, 4]), (12, [2, 3, 2])]
+    for inst in range(20):
+        P, dims = cases[int(rng.integers(len(cases)))]
+        mask = str(int(rng.integers(1, 1 << len(dims))))
+        lb = with_env({"DDL_NVLS_EMULATE": "1", "DDL_NVLS_DIMS": mask}, lambda: ddl.Loopback(P, dims))
+        lb.set_algo(ddl.ALGO_HIER, 0)
+        dtype = ["int32", "float32", "bfloat16"][int(rng.integers(3))]
+        op = "sum" if dtype == "int32" else ["sum", "avg"][int(rng.integers(2))]
+        n = int(rng.choice([8, 64, 1000, 4096, 100_000, 100_003, 777_777]))
+        bufs = si.rank_buffers(dtype, KIND[dtype], n, P, seed=inst)
+        dev = [to_dev(b, dtype) for b in bufs]
+        lb.all_reduce(dev, op)
+        torch.cuda.synchronize()
+        assert lb.async_error() == ddl.SUCCESS
+        outs = [to_host(t) for t in dev]
+        for r in range(P):
+            assert same_bits(outs[r], outs[0]), (inst, dims, mask, dtype, n, r)
+        check(outs[0], bufs, dims, dtype, op, (inst, dims, mask, dtype, op, n))
+        lb.finalize()
