@@ -144,3 +144,35 @@ def test_nvls_emulated_randomized():
             assert same_bits(outs[r], outs[0]), (inst, dims, mask, dtype, n, r)
         check(outs[0], bufs, dims, dtype, op, (inst, dims, mask, dtype, op, n))
         lb.finalize()
+
+
+@pytest.mark.parametrize("P,dims", [(8, [4, 2]), (4, [2, 2]), (8, [2, 2, 2])])
+def test_nvls_emulated_reduce_scatter_allgather(P, dims):
+    """The reduce-scatter and allgather entry points through PATH 7 with the NVLS data flow
+    emulated (loopback and the multi-process path): reduce-scatter slices within the
+    any-order bound (int32 exact), allgather bit-exact (a pure copy)."""
+    recv = 4096 + 64
+    lb = with_env({"DDL_NVLS_EMULATE": "1"}, lambda: ddl.Loopback(P, dims))
+    g = with_env({"DDL_NVLS_EMULATE": "1", "DDL_TIMEOUT_MS": "5000"},
+                 lambda: ddl.InProcessGroup(P, dims, max_bytes=8 << 20))
+    for comm in (lb, g):
+        for dtype in ("int32", "float32", "bfloat16"):
+            op = "sum" if dtype == "int32" else "avg"
+            bufs = si.rank_buffers(dtype, KIND[dtype], P * recv, P, seed=11)
+            sends = [to_dev(b, dtype) for b in bufs]
+            outs = [torch.empty(recv, dtype=TORCH[dtype], device="cuda") for _ in range(P)]
+            comm.reduce_scatter(outs, sends, op)
+            torch.cuda.synchronize()
+            for r in range(P):
+                sl = [b[r * recv:(r + 1) * recv] for b in bufs]
+                check(to_host(outs[r]), sl, dims, dtype, op, ("rs", type(comm).__name__, dims, dtype, r))
+            blocks = si.rank_buffers(dtype, KIND[dtype], recv, P, seed=12)
+            want = oracle.allgather(blocks, dims, dtype)
+            ins = [to_dev(b, dtype) for b in blocks]
+            gat = [torch.empty(P * recv, dtype=TORCH[dtype], device="cuda") for _ in range(P)]
+            comm.all_gather(gat, ins)
+            torch.cuda.synchronize()
+            for r in range(P):
+                assert same_bits(to_host(gat[r]), want[r]), ("ag", type(comm).__name__, dims, dtype, r)
+    lb.finalize()
+    g.finalize()
