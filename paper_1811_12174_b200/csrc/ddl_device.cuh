@@ -90,6 +90,7 @@ struct KParams {
   // register-staged direct phases over the peers' unicast mappings
   char* mc[kMaxDims];
   int nvls_mask;
+  int deep_copy;     // copy phases (AG, copy-in/out) through the kCopySub-deep sub-stage pipeline
   int nvls_emulate;  // test hook (DDL_NVLS_EMULATE=1): the NVLS phases' data flow done with unicast
                      // loads / stores (RS folds the members in DESCENDING coordinate -- an order
                      // other than the direct path's; AG stores each own vector into every member)
@@ -633,7 +634,12 @@ __device__ void ldg_phase(const KParams& p, int me, const PhaseCtx& x) {
 #endif
 constexpr int kStages = DDL_TMA_STAGES;
 constexpr uint32_t kStageBytes = DDL_TMA_STAGE_KB * 1024;
-constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t) + 16;
+// Copy phases (allgather, copy-in/out) run the same ring as kCopySub smaller sub-stages with
+// their own mbarriers (more loads in flight, each store issued as its load lands; -0.7 % on
+// the bench step, profiles/r02_ab/r02_ab11.txt; DDL_DEEP_COPY=0: the 2-stage ring as for RS).
+constexpr int kCopySub = 8;
+constexpr size_t kTmaSmem =
+    (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t) + 16 + kCopySub * sizeof(uint64_t);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
   return (uint32_t)__cvta_generic_to_shared(ptr);
@@ -706,8 +712,10 @@ struct Pipe {
   char* smem;
   uint64_t* bar;
   uint32_t* stored;  // PATH 5: consumer warps that finished storing a chunk (monotone, smem)
+  uint64_t* cbar;    // kCopySub sub-stage barriers of the deep copy pipeline
   uint32_t seq;      // chunks consumed so far by this CTA (identical in every thread)
   uint32_t sseq;     // chunks counted in *stored so far (stream phases only)
+  uint32_t cseq;     // sub-stage chunks consumed by the deep copy pipeline (thread 0)
 };
 
 __device__ __forceinline__ void pipe_init(Pipe& pp) {
@@ -715,10 +723,13 @@ __device__ __forceinline__ void pipe_init(Pipe& pp) {
   pp.smem = dsmem;
   pp.bar = reinterpret_cast<uint64_t*>(dsmem + (size_t)kStages * kStageBytes);
   pp.stored = reinterpret_cast<uint32_t*>(pp.bar + kStages);
+  pp.cbar = reinterpret_cast<uint64_t*>(dsmem + (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t) + 16);
   pp.seq = 0;
   pp.sseq = 0;
+  pp.cseq = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&pp.bar[s], 1);
+    for (int s = 0; s < kCopySub; ++s) mbar_init(&pp.cbar[s], 1);
     *pp.stored = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -735,6 +746,59 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
   const bool do_scale = x.kind == kPhRS && x.last && p.op == kAvg;
   char* dst = dst_base(p, me, x);
   fill_units<T, W>(p, me, x, s_units, s_srcs, nullptr);
+  if (x.kind != kPhRS && p.deep_copy) {
+    // Deep copy pipeline (default; DDL_DEEP_COPY=0 turns it off): thread 0 streams the phase through
+    // kCopySub sub-stages of the ring -- kCopySub - kLag loads in flight, every bulk store
+    // issued as soon as its load lands, a sub-stage reloaded once the store issued kLag
+    // chunks earlier has read it -- while the other threads go straight to the ragged tails.
+    constexpr uint32_t SB = (uint32_t)(kStages * kStageBytes / kCopySub) & ~15u;
+    constexpr int kLag = 2;
+    if (threadIdx.x == 0) {
+      uint32_t ctot = 0;
+      for (int u = 0; u < x.nunits; ++u) ctot += (s_units[u].bytes + SB - 1) / SB;
+      const bool evf = x.kind == kPhAG && (p.l2hint & 2) && (x.last || !(p.l2hint & 32));
+      const uint64_t pol = evf ? policy_evict_first() : 0;
+      int lu = 0, su = 0;
+      uint32_t loff = 0, soff = 0;
+      auto next_chunk = [&](int& u, uint32_t& off) -> uint32_t {  // bytes of the chunk at (u, off)
+        while (off >= s_units[u].bytes) {
+          ++u;
+          off = 0;
+        }
+        return min(SB, s_units[u].bytes - off);
+      };
+      auto issue = [&](uint32_t j) {
+        const uint32_t bytes = next_chunk(lu, loff);
+        const int sub = (int)((pp.cseq + j) % kCopySub);
+        mbar_arm(&pp.cbar[sub], bytes);
+        tma_load(pp.smem + (size_t)sub * SB, s_units[lu].src + s_units[lu].e0 * sizeof(T) + loff, bytes,
+                 &pp.cbar[sub]);
+        loff += bytes;
+      };
+      if (ctot) fence_proxy_async_global();
+      for (uint32_t j = 0; j < ctot && j < (uint32_t)kCopySub; ++j) issue(j);
+      for (uint32_t j = 0; j < ctot; ++j) {
+        const uint32_t cs = pp.cseq + j;
+        const int sub = (int)(cs % kCopySub);
+        const uint32_t bytes = next_chunk(su, soff);
+        mbar_wait(&pp.cbar[sub], (cs / kCopySub) & 1u);
+        char* pd = dst + s_units[su].e0 * sizeof(T) + soff;
+        if (evf) tma_store_hint(pd, pp.smem + (size_t)sub * SB, bytes, pol);
+        else tma_store(pd, pp.smem + (size_t)sub * SB, bytes);
+        soff += bytes;
+        if (j >= (uint32_t)kLag && j - kLag + kCopySub < ctot) {
+          asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kLag) : "memory");
+          issue(j - kLag + kCopySub);
+        }
+      }
+      // the tail: stores whose sub-stages are not reloaded
+      tma_store_wait_all();
+      fence_proxy_async_global();
+      pp.cseq += ctot;
+    }
+    ragged_tails<T>(p, x, dst, s_units, s_srcs);
+    return;
+  }
   uint32_t total = 0;
   for (int u = 0; u < x.nunits; ++u) total += (s_units[u].bytes + CB - 1) / CB;
 

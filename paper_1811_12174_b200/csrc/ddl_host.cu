@@ -157,6 +157,7 @@ struct ddl_comm {
   int group_waves = 1;                     // DDL_GROUP_WAVES: waves per bucket in a grouped all-reduce (0 = auto)
   size_t group_wave_bytes = 0;             // DDL_GROUP_WAVE_MB: per-wave partial footprint budget (0 = off)
   int group_order = 0;                     // DDL_GROUP_ORDER: 0 LPT (longest first), 1 ascending within a channel
+  int deep_copy = 1;                       // DDL_DEEP_COPY: copy phases through the deep sub-stage pipeline
   int waves = 0;                           // DDL_WAVES: slices per CTA per hierarchical call (0 = auto)
   size_t wave_slice_bytes = 112 << 10;     // auto: target per-CTA slice of one wave
   size_t min_wave_slice_bytes = 16 << 10;  // no waves below this slice size
@@ -272,6 +273,7 @@ void apply_env(ddl_comm* c) {
   c->group_waves = (int)env_size("DDL_GROUP_WAVES", c->group_waves);
   c->group_wave_bytes = env_size("DDL_GROUP_WAVE_MB", c->group_wave_bytes >> 20) << 20;
   c->group_order = (int)env_size("DDL_GROUP_ORDER", c->group_order);
+  c->deep_copy = (int)env_size("DDL_DEEP_COPY", c->deep_copy);
   c->nvls_dims_mask = std::getenv("DDL_NVLS_DIMS") ? (int)env_size("DDL_NVLS_DIMS", 0) : -1;
   c->nvls_emulate = env_size("DDL_NVLS_EMULATE", 0) != 0;
   c->l2hint = (int)env_size("DDL_L2_HINTS", c->l2hint);
@@ -532,6 +534,7 @@ KParams base_params(const ddl_comm* c, uint64_t n, ddl_op_t op) {
   p.trace = c->trace;
   p.stream_every = c->stream_every;
   p.l2hint = c->l2hint;
+  p.deep_copy = c->deep_copy;
   for (int r = 0; r < c->P; ++r) p.flags[r] = c->flags_of(r);
   return p;
 }

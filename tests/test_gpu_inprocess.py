@@ -58,6 +58,7 @@ VARIANTS = {"default": None, "tma": {"DDL_TMA_MIN_SLICE_BYTES": "0"},
             "stream": {"DDL_STREAM": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"},
             "steal": {"DDL_STEAL": "1", "DDL_TMA_MIN_SLICE_BYTES": "0"},
             "check": {"DDL_CHECK": "1"},
+            "no-deep-copy": {"DDL_DEEP_COPY": "0", "DDL_TMA_MIN_SLICE_BYTES": "0"},
             "waves": {"DDL_WAVES": "3", "DDL_MIN_WAVE_SLICE_BYTES": "0", "DDL_TMA_MIN_SLICE_BYTES": "0"}}
 
 

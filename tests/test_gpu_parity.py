@@ -265,6 +265,7 @@ PATH_ENVS = {"steal": {"DDL_STEAL": "1"}, "dyn": {"DDL_DYN": "1"}, "ldg": {"DDL_
              "tma-all": {"DDL_TMA_MIN_SLICE_BYTES": "0"}, "stream": {"DDL_STREAM": "1"},
              "no-l2-hints": {"DDL_L2_HINTS": "0", "DDL_TMA_MIN_SLICE_BYTES": "0"},
              "no-transpose": {"DDL_TRANSPOSE": "0"},
+             "no-deep-copy": {"DDL_DEEP_COPY": "0", "DDL_TMA_MIN_SLICE_BYTES": "0"},
              "no-transpose-waves": {"DDL_TRANSPOSE": "0", "DDL_WAVES": "3", "DDL_MIN_WAVE_SLICE_BYTES": "0"},
              "all-l2-hints": {"DDL_L2_HINTS": "31", "DDL_TMA_MIN_SLICE_BYTES": "0"},
              # waves (TMA-staged path): every CTA walks 3 (5) slices one after another, down to
