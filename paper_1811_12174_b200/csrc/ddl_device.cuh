@@ -637,7 +637,13 @@ constexpr uint32_t kStageBytes = DDL_TMA_STAGE_KB * 1024;
 // Copy phases (allgather, copy-in/out) run the same ring as kCopySub smaller sub-stages with
 // their own mbarriers (more loads in flight, each store issued as its load lands; -0.7 % on
 // the bench step, profiles/r02_ab/r02_ab11.txt; DDL_DEEP_COPY=0: the 2-stage ring as for RS).
-constexpr int kCopySub = 8;
+#ifndef DDL_COPY_SUB
+#define DDL_COPY_SUB 8
+#endif
+#ifndef DDL_COPY_LAG
+#define DDL_COPY_LAG 2
+#endif
+constexpr int kCopySub = DDL_COPY_SUB;
 constexpr size_t kTmaSmem =
     (size_t)kStages * kStageBytes + kStages * sizeof(uint64_t) + 16 + kCopySub * sizeof(uint64_t);
 
@@ -752,7 +758,7 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
     // issued as soon as its load lands, a sub-stage reloaded once the store issued kLag
     // chunks earlier has read it -- while the other threads go straight to the ragged tails.
     constexpr uint32_t SB = (uint32_t)(kStages * kStageBytes / kCopySub) & ~15u;
-    constexpr int kLag = 2;
+    constexpr int kLag = DDL_COPY_LAG;
     if (threadIdx.x == 0) {
       uint32_t ctot = 0;
       for (int u = 0; u < x.nunits; ++u) ctot += (s_units[u].bytes + SB - 1) / SB;
