@@ -47,10 +47,32 @@ TRAFFIC_KEY = "resnet50-grad-set 8 virtual ranks dims 2x4 avg, grouped"
 
 
 def source_hash() -> str:
-    """sha256 of the DEVICE sources libddl.so's kernels are compiled from (the .cuh kernel
-    files, the shared planner header, build.sh's flags): ties a committed ncu capture of a
-    kernel's DRAM traffic to the kernel code it measured."""
+    """Identity of the kernels a committed ncu capture measured: sha256 of libddl.so's SASS
+    (cuobjdump, addresses and encodings stripped) -- so a source edit that compiles to the same
+    machine code keeps the capture valid and any kernel change invalidates it; without
+    cuobjdump, sha256 of the device sources (.cuh kernel files, planner header, build.sh)."""
     import hashlib
+    import re
+    lib = os.path.join(ROOT, "paper_1811_12174_b200", "libddl.so")
+    side = lib + ".sass-sha"   # written by build.sh right after the build (cuobjdump takes ~10 s)
+    try:
+        if os.path.getmtime(side) >= os.path.getmtime(lib):
+            return open(side).read().strip()
+    except OSError:
+        pass
+    try:
+        sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, timeout=120).stdout
+        ins = re.findall(r"^\s+/\*[0-9a-f]+\*/\s+(.*?;)", sass, flags=re.M)
+        if ins:
+            hv = "sass-" + hashlib.sha256("\n".join(ins).encode()).hexdigest()[:16]
+            try:
+                with open(side, "w") as f:
+                    f.write(hv + "\n")
+            except OSError:
+                pass
+            return hv
+    except Exception:
+        pass
     h = hashlib.sha256()
     src = os.path.join(ROOT, "paper_1811_12174_b200", "csrc")
     for name in sorted(f for f in os.listdir(src) if f.endswith(".cuh")) + ["ddl_plan.h", "../../build.sh"]:

@@ -29,6 +29,9 @@
 
 namespace ddl {
 
+#ifndef DDL_MUTATE
+#define DDL_MUTATE 0  // 1-3: deliberately wrong kernels for scripts/gpu_mutation_check.sh (never in a product build)
+#endif
 constexpr int kThreads = 512;
 constexpr int kMaxLocalIn = 64;
 
@@ -782,6 +785,9 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
         loff += bytes;
       };
       if (ctot) fence_proxy_async_global();
+#if DDL_MUTATE == 3  // mutation check: every copy phase drops its last chunk
+      if (ctot > 1) --ctot;
+#endif
       for (uint32_t j = 0; j < ctot && j < (uint32_t)kCopySub; ++j) issue(j);
       for (uint32_t j = 0; j < ctot; ++j) {
         const uint32_t cs = pp.cseq + j;
@@ -859,14 +865,23 @@ __device__ void tma_phase(const KParams& p, int me, const PhaseCtx& x, Pipe& pp)
       const uint64_t pol_last = keep ? policy_evict_last() : 0;
       for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
         A acc[W];
+#if DDL_MUTATE == 1  // mutation check (scripts/gpu_mutation_check.sh): fold the members in descending order
+        unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)(x.g - 1) * CB + (size_t)i * 16), acc);
+        for (int v = x.g - 2; v >= 0; --v) {
+#else
         unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)i * 16), acc);
         for (int v = 1; v < x.g; ++v) {
+#endif
           A y[W];
           unpack<T>(*reinterpret_cast<const uint4*>(sbase + (size_t)v * CB + (size_t)i * 16), y);
 #pragma unroll
           for (int k = 0; k < W; ++k) acc[k] = Tr<T>::add(acc[k], y[k]);
         }
+#if DDL_MUTATE == 2  // mutation check: the fused 1/P scale dropped
+        if (false) {
+#else
         if (do_scale) {
+#endif
 #pragma unroll
           for (int k = 0; k < W; ++k) acc[k] = Tr<T>::mul(acc[k], p.scale);
         }
