@@ -8,8 +8,10 @@ gradient set: the BASELINE.json configs[1] workload, ResNet-50's 25.6M fp32 grad
 its 5 DDP buckets, all-reduced with op=avg, dims 2x4 (= [4, 2]).
 
 * N = 1 (no torchrun): LOOPBACK -- the 8 ranks of the 2x4 factorisation are virtual ranks
-  on one B200 (one cooperative launch per bucket, the same kernels / block layout / barrier
-  protocol as the multi-GPU path, peer pointers local).  Bound: HBM.
+  on one B200, all in one HBM.  The step runs through the loopback column-chain kernel
+  (ddl_chain.cuh: every RS / AG phase of the schedule, per column, in one thread; one launch
+  for the 5 buckets); the multi-GPU path's per-CTA slice kernel with device barriers
+  (ddl_multi_kernel) is timed on the same step beside it (`slice_kernel`).  Bound: HBM.
 * N > 1 (torchrun, one process per GPU): real ranks, peers' buffers mapped over NVLink 5 /
   NVSwitch, dims 8 -> 2x4, 4 -> 2x2, 2 -> 2.  Bound: NVLink.  NCCL's all-reduce on the same
   buffers is timed alongside (comparison only).
@@ -264,7 +266,7 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- value gate
-def value_gate(lb, sizes, P, dims, dev, bufs):
+def value_gate(lb, sizes, P, dims, dev, bufs, slice_lb=None):
     """Before any timing, the exact step call is checked on VALUES, not only on agreement
     between ranks (a schedule that drops or doubles one rank the same way everywhere would
     still agree):
@@ -303,8 +305,19 @@ def value_gate(lb, sizes, P, dims, dev, bufs):
     for b in range(len(sizes)):
         assert all(torch.equal(x.view(torch.int32), y.view(torch.int32)) for x, y in zip(a[b], s_[b])), \
             f"grouped != single calls, bucket {b}"
+    # 3. the column-chain kernel == the slice kernels with device barriers (the multi-GPU path's
+    #    kernels, DDL_LB_CHAIN=0), bit for bit on the step's inputs
+    if slice_lb is not None:
+        c_ = [[t.clone() for t in bk] for bk in bufs]
+        slice_lb.all_reduce_many(c_, "avg")
+        torch.cuda.synchronize()
+        for b in range(len(sizes)):
+            assert all(torch.equal(x.view(torch.int32), y.view(torch.int32)) for x, y in zip(a[b], c_[b])), \
+                f"chain kernel != slice kernel, bucket {b}"
+        del c_
     return ("closed forms (fp32 r+1 avg, int32 bitmask sum) through the grouped call on the step's bucket "
-            "sizes; grouped step == 5 single calls bitwise; all ranks identical after warm-up")
+            "sizes; grouped step == 5 single calls bitwise; column-chain kernel == barrier slice kernel bitwise; "
+            "all ranks identical after warm-up")
 
 
 # ----------------------------------------------------------------------------- N = 1: loopback
@@ -317,6 +330,13 @@ def run_loopback(args):
     P = 8
     dims = ddl.parse_dims(args.dims or DIMS_FOR_N[1])
     lb = ddl.Loopback(P, dims, device=0)
+    # the same step through the per-CTA slice kernels with device barriers (the kernels the
+    # multi-GPU path runs; context, timed after the headline)
+    os.environ["DDL_LB_CHAIN"] = "0"
+    try:
+        slice_lb = ddl.Loopback(P, dims, device=0)
+    finally:
+        os.environ.pop("DDL_LB_CHAIN", None)
     host = [resnet50_set(r) for r in range(P)]                 # [rank][bucket]
     nb = len(host[0])
     sizes = [h.size for h in host[0]]
@@ -338,7 +358,7 @@ def run_loopback(args):
             if evs is not None:
                 evs[b][1].record(stream)
 
-    gate = value_gate(lb, sizes, P, dims, dev, bufs)
+    gate = value_gate(lb, sizes, P, dims, dev, bufs, slice_lb)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:   # sampling spans warm-up + timed region (>= a few 100-ms samples)
         for _ in range(args.warmup):
@@ -375,8 +395,17 @@ def run_loopback(args):
         for k in range(args.steps):
             seq_step()
         s1.record(stream)
+        # context: the same grouped step through the slice kernel with device barriers
+        for _ in range(2):
+            slice_lb.all_reduce_many(bufs, "avg")
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for k in range(args.steps):
+            slice_lb.all_reduce_many(bufs, "avg")
+        m1.record(stream)
         torch.cuda.synchronize()
-    assert lb.async_error() == ddl.SUCCESS
+    assert lb.async_error() == ddl.SUCCESS and slice_lb.async_error() == ddl.SUCCESS
+    slice_ms = m0.elapsed_time(m1) / args.steps
     ms = t_start.elapsed_time(t_end) / args.steps
     busbw = S_total * 2 * (P - 1) / P / (ms * 1e-3) / 1e9
     kern_ms = sum(kev[k][0].elapsed_time(kev[k][1]) for k in range(args.steps))
@@ -450,12 +479,19 @@ def run_loopback(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_key(P, dims),
-                   "ranks": "8 virtual ranks on one B200 (loopback: same kernels and barrier protocol)",
+                   "ranks": "8 virtual ranks on one B200 (loopback: the column-chain kernel runs every phase "
+                            "of the schedule per column in one thread)",
                    "dims": "x".join(map(str, dims[::-1])), "n_ranks": P, "bytes_per_rank": S_total,
                    "buckets": sizes, "l2": "inputs (8 x 102 MB) larger than L2, no flush",
                    "algo": ["oneshot" if lb.algo_for(s, "float32") == ddl.ALGO_ONESHOT else "hier" for s in sizes],
-                   "step": "one grouped all-reduce of the 5 buckets (ddl_group_allreduce_many, "
-                           f"{os.environ.get('DDL_CHANNELS', '2')} channels, {launches_per_step} launch(es))",
+                   "step": "one grouped all-reduce of the 5 buckets (ddl_group_allreduce_many, column-chain "
+                           f"kernel, {launches_per_step} launch(es))",
+                   "slice_kernel": {"ms_per_step": round(slice_ms, 4),
+                                    "value": S_total * 2 * (P - 1) / P / (slice_ms * 1e-3) / 1e9,
+                                    "frac": 2 * P * S_total / (slice_ms * 1e-3) / 1e9 / hbm_peak,
+                                    "kernel": "ddl_multi_kernel<float> (the multi-GPU path's per-CTA slice "
+                                              "kernel with device barriers, DDL_LB_CHAIN=0; same step, "
+                                              "bit-identical results, checked in the gate)"},
                    "sequential": {"ms_per_step": round(seq_ms, 4), "calls": "5 single ddl_group_allreduce",
                                   "ctas_per_rank": [lb.ctas_for(s, "float32") for s in sizes],
                                   "bucket_us": [round(u, 1) for u in bucket_us]}},
@@ -467,8 +503,8 @@ def run_loopback(args):
                                      "(null unless that capture measured this build: source hash)",
                      "algorithmic_bytes_per_launch": algo_bytes // args.steps // launches_per_step,
                      "peak_source": peak_src,
-                     "kernel": "ddl_multi_kernel<float> (grouped: 5 buckets x 8 virtual ranks in one launch, "
-                               "TMA-staged phases)",
+                     "kernel": "ddl_chain_ct_kernel<float, CT<2,4,2>> (loopback column chain: 5 buckets x 8 "
+                               "virtual ranks in one launch, every RS/AG phase per column in one thread)",
                      "kernel_timing": "second pass of K steps, CUDA events around every launch",
                      "algorithmic_bytes": "compulsory: 2 x 8 virtual ranks x 102,228,128 B per step "
                                           "(each input read once, each result written once)",
@@ -493,6 +529,7 @@ def run_loopback(args):
         line["cpu_baseline"] = oracle_baseline(P, dims, host)
     print(json.dumps(line), flush=True)
     lb.finalize()
+    slice_lb.finalize()
 
 
 # ----------------------------------------------------------------------------- N > 1

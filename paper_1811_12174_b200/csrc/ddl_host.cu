@@ -16,6 +16,7 @@
 
 #include "ddl.h"
 #include "ddl_device.cuh"
+#include "ddl_chain.cuh"
 #include "ddl_plan.h"
 #include "ddl_nvls.h"
 
@@ -165,6 +166,10 @@ struct ddl_comm {
   bool force_sys = false;  // DDL_FORCE_SYS_SCOPE=1: .sys flags even when every rank shares this GPU
   bool debug = false;      // DDL_DEBUG: one stderr line per launch
   int stream_every = 1;    // DDL_STREAM_EVERY (PATH 5)
+  int lb_chain = 1;        // DDL_LB_CHAIN: loopback all-reduces through the column-chain kernel (0: the
+                           // per-CTA slice kernels with device barriers, as across processes)
+  int chain_hint = 0;      // DDL_CHAIN_HINTS: CParams::hint bits (generic chain kernel)
+  bool chain_generic = false;  // DDL_CHAIN_GENERIC=1: the generic chain kernel also where a CT kernel exists
 
   uint32_t* flags_of(int r) const {
     if (loopback) return reinterpret_cast<uint32_t*>(lb_flags + (size_t)r * flags_bytes);
@@ -213,10 +218,11 @@ namespace {
 
 // Launch with the optional cooperative (loopback: all P x nctas CTAs co-resident) and
 // programmatic-dependent-launch attributes (every kernel starts with pdl_begin()).
-cudaError_t launch_ex(const void* fn, dim3 grid, size_t smem, cudaStream_t s, void** args, bool coop, bool pdl) {
+cudaError_t launch_ex(const void* fn, dim3 grid, size_t smem, cudaStream_t s, void** args, bool coop, bool pdl,
+                      int threads = kThreads) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -242,7 +248,7 @@ bool pdl_default() {
 }
 
 // Resident CTAs (kThreads each) per SM for a kernel, cached.
-int blocks_per_sm(const void* fn, size_t smem = 0) {
+int blocks_per_sm(const void* fn, size_t smem = 0, int threads = kThreads) {
   static std::mutex mu;
   static std::unordered_map<const void*, int> cache;
   std::lock_guard<std::mutex> lk(mu);
@@ -250,7 +256,7 @@ int blocks_per_sm(const void* fn, size_t smem = 0) {
   if (it != cache.end()) return it->second;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess) nb = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess) nb = 1;
   if (nb < 1) nb = 1;
   cache[fn] = nb;
   return nb;
@@ -288,6 +294,9 @@ void apply_env(ddl_comm* c) {
   c->force_sys = env_size("DDL_FORCE_SYS_SCOPE", 0) != 0;
   c->debug = std::getenv("DDL_DEBUG") != nullptr;
   c->stream_every = (int)env_size("DDL_STREAM_EVERY", 1);
+  c->lb_chain = (int)env_size("DDL_LB_CHAIN", c->lb_chain);
+  c->chain_hint = (int)env_size("DDL_CHAIN_HINTS", c->chain_hint);
+  c->chain_generic = env_size("DDL_CHAIN_GENERIC", 0) != 0;
   if (c->stream_every < 1) c->stream_every = 1;
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
@@ -645,6 +654,109 @@ ddl_result_t nvls_allreduce(const ddl_comm* c, KParams& p, void* buf, size_t cou
     p.mode = kRS | kAG;
   }
   return launch(c, p, pl, dt, stream);
+}
+
+// ---------------------------------------------------------------- loopback column-chain kernel
+// (ddl_chain.cuh) The loopback all-reduce (single or grouped) as independent columns, each
+// running the whole schedule in one thread.  Not used with the debug hooks that need the
+// slice kernels' barriers (skip_rank, trace), the NVLS emulation or the experiment variants.
+bool use_chain(const ddl_comm* c) {
+  return c->loopback && c->lb_chain && c->skip_rank < 0 && !c->trace && !c->nvls_emulate && !c->use_dyn &&
+         !c->use_steal && !c->use_stream;
+}
+
+// Column-chain kernels: a compile-time-topology kernel (rows of P columns) for the live-dim
+// sequences of P = 2, 4, 8; the generic kernel (one column per thread) otherwise (at P = 16
+// the compile-time kernel's P-wide register arrays spill).
+template <typename T>
+const void* chain_ct_t(const Topo& t) {
+  int g[4] = {1, 1, 1, 1};
+  const int L = t.nlive;
+  if (L < 1 || L > 4) return nullptr;
+  for (int l = 0; l < L; ++l) g[l] = t.g[t.live[l]];
+#define DDL_CT(L_, a, b, c, d)                                               \
+  if (L == L_ && g[0] == a && g[1] == b && g[2] == c && g[3] == d)          \
+    return (const void*)ddl_chain_ct_kernel<T, CT<L_, a, b, c, d>>;
+  DDL_CT(1, 2, 1, 1, 1)
+  DDL_CT(1, 4, 1, 1, 1) DDL_CT(2, 2, 2, 1, 1)
+  DDL_CT(1, 8, 1, 1, 1) DDL_CT(2, 4, 2, 1, 1) DDL_CT(2, 2, 4, 1, 1) DDL_CT(3, 2, 2, 2, 1)
+#undef DDL_CT
+  return nullptr;
+}
+template <typename T>
+const void* chain_fn_t(const Topo& t, bool generic, bool* ct) {
+  if (!generic) {
+    if (const void* f = chain_ct_t<T>(t)) {
+      *ct = true;
+      return f;
+    }
+  }
+  *ct = false;
+  if (t.P <= 4) return (const void*)ddl_chain_kernel<T, 4>;
+  if (t.P <= 8) return (const void*)ddl_chain_kernel<T, 8>;
+  return (const void*)ddl_chain_kernel<T, 16>;
+}
+const void* chain_fn_dt(ddl_dtype_t dt, const Topo& t, bool generic, bool* ct) {
+  if (dt == DDL_INT32) return chain_fn_t<int32_t>(t, generic, ct);
+  if (dt == DDL_FLOAT32) return chain_fn_t<float>(t, generic, ct);
+  return chain_fn_t<__nv_bfloat16>(t, generic, ct);
+}
+
+// Buffers i < nb with counts ns[i] and every rank's pointer ptrs[i * P + m]: their columns
+// (P blocks of q / W vectors each) concatenated, at most kMaxBuckets buffers and 2^31 columns
+// per launch; one persistent grid (resident CTAs x SMs) walks them grid-stride.
+ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* ptrs, int nb, ddl_dtype_t dt,
+                                 ddl_op_t op, void* stream) {
+  bool ct = false;
+  const void* fn = chain_fn_dt(dt, c->topo, c->chain_generic, &ct);
+  const int w = elem_size(dt);
+  const uint64_t W = 16 / w;
+  const uint64_t kMaxCols = 1ull << 31;
+  int i = 0;
+  while (i < nb) {
+    CParams cp;
+    std::memset(&cp, 0, sizeof(cp));
+    cp.t = c->topo;
+    cp.op = op;
+    cp.scale = 1.0f / (float)c->P;  // fl32(1/P)
+    cp.hint = c->chain_hint;
+    uint64_t cols = 0, rows = 0;
+    while (i < nb && cp.nb < kMaxBuckets) {
+      const uint64_t n = ns[i];
+      const uint64_t q = block_elems(n, c->P, w);
+      const uint64_t vq = q / W;
+      // CT kernels: rows v < vfull have a whole vector in every block (the last block holds
+      // n - (P-1) q elements); the other rows' columns go through the generic column code
+      const uint64_t last = n > (uint64_t)(c->P - 1) * q ? n - (uint64_t)(c->P - 1) * q : 0;
+      const uint64_t vfull = ct ? std::min<uint64_t>(vq, last / W) / kChainVPT * kChainVPT : 0;
+      const uint64_t bc = (uint64_t)c->P * (vq - vfull);
+      if (bc > kMaxCols || vfull > kMaxCols) return DDL_ERR_TOO_LARGE;
+      if (cols + bc > kMaxCols || rows + vfull > kMaxCols) break;
+      CBucket& B = cp.b[cp.nb++];
+      B.n = n;
+      B.q = q;
+      B.vq = (uint32_t)vq;
+      B.vfull = (uint32_t)vfull;
+      B.col0 = (uint32_t)cols;
+      B.row0 = (uint32_t)rows;
+      for (int m = 0; m < c->P; ++m) B.buf[m] = static_cast<char*>(ptrs[(size_t)i * c->P + m]);
+      cols += bc;
+      rows += vfull;
+      ++i;
+    }
+    cp.ncols = (uint32_t)cols;
+    cp.nrows = (uint32_t)rows;
+    if (!cols && !rows) continue;
+    const uint64_t need = (std::max(rows / kChainVPT, ct ? 0 : cols) + kChainThreads - 1) / kChainThreads;
+    const uint64_t cap = (uint64_t)blocks_per_sm(fn, 0, kChainThreads) * c->num_sms;
+    const int grid = (int)std::max<uint64_t>(1, std::min(need, c->ctas_limit > 0 ? (uint64_t)c->ctas_limit : cap));
+    if (c->debug)
+      std::fprintf(stderr, "[ddl] chain%s: %d buffers, %llu columns, grid %d\n", ct ? " (ct)" : "", cp.nb,
+                   (unsigned long long)cols, grid);
+    void* args[] = {&cp};
+    DDL_CUDA(launch_ex(fn, dim3(grid), 0, static_cast<cudaStream_t>(stream), args, false, c->use_pdl, kChainThreads));
+  }
+  return DDL_SUCCESS;
 }
 
 ddl_result_t check_common(const ddl_comm* c, ddl_dtype_t dt, ddl_op_t op) {
@@ -1711,6 +1823,13 @@ static void preload_kernels() {
         for (int R : {1, 2, 4}) fns.push_back(oneshot_fn_dt(dt, K, R));
       }
       fns.push_back(multi_fn_dt(dt));
+      for (int P : {2, 4, 6, 8, 16}) {  // the flat topology's kernel per P (CT for 2, 4, 8; generic else)
+        Topo t;
+        make_topo(&t, P, &P, 1);
+        bool ct;
+        fns.push_back(chain_fn_dt(dt, t, false, &ct));
+        fns.push_back(chain_fn_dt(dt, t, true, &ct));
+      }
     }
     fns.push_back((const void*)ddl_local_reduce_kernel<int32_t, true>);
     fns.push_back((const void*)ddl_local_reduce_kernel<int32_t, false>);
@@ -1744,7 +1863,7 @@ ddl_result_t ddl_group_allreduce_many(ddl_comm_t c, void* const* bufs, const siz
   for (int i = 0; i < nbufs; ++i) {
     if (!counts[i]) continue;
     Plan pl;
-    if (!grouped_kernel_ok(c) || use_oneshot(c, counts[i], dt, &pl)) {
+    if ((!grouped_kernel_ok(c) && !use_chain(c)) || use_oneshot(c, counts[i], dt, &pl)) {
       if ((r = ddl_group_allreduce(c, bufs + (size_t)i * c->P, counts[i], dt, op, stream)) != DDL_SUCCESS) return r;
       continue;
     }
@@ -1752,6 +1871,7 @@ ddl_result_t ddl_group_allreduce_many(ddl_comm_t c, void* const* bufs, const siz
     for (int m = 0; m < c->P; ++m) ptrs.push_back(bufs[(size_t)i * c->P + m]);
   }
   if (ns.empty()) return DDL_SUCCESS;
+  if (use_chain(c)) return launch_chain(c, ns.data(), ptrs.data(), (int)ns.size(), dt, op, stream);
   return launch_multi(c, ns.data(), ptrs.data(), (int)ns.size(), dt, op, stream);
 }
 
@@ -1806,6 +1926,10 @@ ddl_result_t ddl_group_allreduce(ddl_comm_t c, void* const* bufs, size_t count, 
     return launch(c, p, pl, dt, stream);
   }
   const bool one = use_oneshot(c, count, dt, &pl);
+  if (!one && use_chain(c)) {
+    const uint64_t n = count;
+    return launch_chain(c, &n, bufs, 1, dt, op, stream);
+  }
   if (!one) pl = plan_hier(c, count, block_elems(count, c->P, elem_size(dt)), dt, true);
   p.q = pl.q;
   p.slice = pl.slice;

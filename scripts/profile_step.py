@@ -1,7 +1,9 @@
 """Run the bench.py N=1 workload (ResNet-50 gradient set, 8 virtual ranks, dims 2x4, avg)
 for W warm-up steps + 1 step, nothing else -- the target of the ncu captures (one grouped
 launch per step):
-  ncu --set full -k regex:ddl_multi -s W -c 1 python scripts/profile_step.py --warmup W"""
+  ncu --set full -k regex:ddl_chain -s W -c 1 python scripts/profile_step.py --warmup W
+(the loopback step runs the column-chain kernel; DDL_LB_CHAIN=0 and -k regex:ddl_multi profile
+the slice kernel instead)"""
 import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

@@ -7,7 +7,7 @@ timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TA
 timeout 300 python bench.py 2>&1 | tail -1 > gpurun_out/${TAG}_bench.json
 timeout 300 python bench.py --impl reference 2>&1 | tail -1 > gpurun_out/${TAG}_bench_reference.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:ddl_multi -s 3 -c 1 -f -o gpurun_out/${TAG}_step python scripts/profile_step.py --warmup 3 > gpurun_out/${TAG}_step.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ddl_chain -s 3 -c 1 -f -o gpurun_out/${TAG}_step python scripts/profile_step.py --warmup 3 > gpurun_out/${TAG}_step.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:local_reduce -s 3 -c 1 -f -o gpurun_out/${TAG}_k5 python scripts/profile_k5.py --warmup 3 > gpurun_out/${TAG}_k5.log 2>&1
 cat gpurun_out/${TAG}_pytest_gpu.txt gpurun_out/${TAG}_smoke.txt
 python -c "import json; d=json.load(open('gpurun_out/${TAG}_bench.json')); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['e2e']['value'], d['clocks'], d['local_reduce'])"

@@ -384,15 +384,16 @@ def test_slice_over_1gib_cut_into_waves():
     message whose per-CTA slice exceeds 1 GiB, the call is cut into waves (or refused with
     DDL_ERR_TOO_LARGE), never silently wrapped: every element of a 2-rank int32 all-reduce
     of 2^29 + 64 elements per rank equals the closed form."""
-    old = os.environ.get("DDL_CTAS")
-    os.environ["DDL_CTAS"] = "1"
+    old = {k: os.environ.get(k) for k in ("DDL_CTAS", "DDL_LB_CHAIN")}
+    os.environ.update({"DDL_CTAS": "1", "DDL_LB_CHAIN": "0"})  # the slice kernels' 32-bit fields
     try:
         lb = ddl.Loopback(2, [2])
     finally:
-        if old is None:
-            os.environ.pop("DDL_CTAS", None)
-        else:
-            os.environ["DDL_CTAS"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     lb.set_algo(ddl.ALGO_HIER, 0)
     n = (1 << 29) + 64
     bufs = [torch.full((n,), r + 1, dtype=torch.int32, device="cuda") for r in range(2)]

@@ -52,10 +52,13 @@ def make(P, dtype, sizes, seed):
     return hosts, devs
 
 
+@pytest.mark.parametrize("kernel", ["chain", "slice"])
 @pytest.mark.parametrize("P,dims", [(8, [4, 2]), (8, [2, 2, 2]), (8, [8]), (4, [2, 2]), (6, [3, 2])])
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-def test_loopback_grouped_matches_oracle(P, dims, dtype):
-    lb = ddl.Loopback(P, dims)
+def test_loopback_grouped_matches_oracle(P, dims, dtype, kernel):
+    """The grouped loopback call through the column-chain kernel (default) and through the
+    grouped slice kernel (DDL_LB_CHAIN=0, the multi-process path's ddl_multi_kernel)."""
+    lb = with_env({"DDL_LB_CHAIN": "0" if kernel == "slice" else "1"}, lambda: ddl.Loopback(P, dims))
     op = "sum" if dtype == "int32" else "avg"
     hosts, devs = make(P, dtype, SIZES, seed=100)
     lb.all_reduce_many(devs, op)
@@ -72,7 +75,7 @@ def test_loopback_grouped_channels_and_split(channels, waves, transpose):
     waves per bucket (DDL_GROUP_WAVES, 0 = auto), transposed grid or not."""
     P, dims = 8, [4, 2]
     lb = with_env({"DDL_CHANNELS": channels, "DDL_GROUP_WAVES": waves, "DDL_MIN_WAVE_SLICE_BYTES": "0",
-                   "DDL_TRANSPOSE": transpose}, lambda: ddl.Loopback(P, dims))
+                   "DDL_TRANSPOSE": transpose, "DDL_LB_CHAIN": "0"}, lambda: ddl.Loopback(P, dims))
     sizes = [200_003 + 37_011 * i for i in range(11)]
     hosts, devs = make(P, "float32", sizes, seed=7)
     lb.all_reduce_many(devs, "sum")
@@ -183,7 +186,7 @@ def test_grouped_honours_kernel_variant(env):
     if "DDL_STEAL" in env and not ddl.has_experimental_kernels():
         pytest.skip("PATH 4 not compiled (DDL_EXPERIMENTAL=1 bash build.sh)")
     P, dims = 8, [4, 2]
-    lb = with_env(env, lambda: ddl.Loopback(P, dims))
+    lb = with_env(dict(env, DDL_LB_CHAIN="0"), lambda: ddl.Loopback(P, dims))
     hosts, devs = make(P, "float32", SIZES, seed=500)
     lb.all_reduce_many(devs, "avg")
     torch.cuda.synchronize()
@@ -257,7 +260,7 @@ def test_grouped_randomized_instances():
         nbk = int(rng.integers(1, 9))
         sizes = [int(rng.choice([0, 1, 17, 5000, 70_001, 300_000, 999_983])) for _ in range(nbk)]
         env = {"DDL_CHANNELS": str(int(rng.integers(1, 5))), "DDL_GROUP_WAVES": str(int(rng.integers(1, 4))),
-               "DDL_MIN_WAVE_SLICE_BYTES": "0"}
+               "DDL_MIN_WAVE_SLICE_BYTES": "0", "DDL_LB_CHAIN": str(inst % 2)}  # slice kernel / chain kernel
         lb = with_env(env, lambda: ddl.Loopback(P, dims))
         hosts, devs = make(P, dtype, sizes, seed=9000 + 10 * inst)
         lb.all_reduce_many(devs, op)

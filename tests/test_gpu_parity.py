@@ -42,11 +42,26 @@ def factorisations(P, maxlen=4):
 
 _LB = {}
 
+# loopback kernels: "chain" (default: the column-chain kernel, ddl_chain.cuh) and "slice" (the
+# per-CTA slice kernels with device barriers, DDL_LB_CHAIN=0 -- the multi-process path's kernels)
+LB_KERNELS = {"chain": {}, "slice": {"DDL_LB_CHAIN": "0"}}
 
-def loopback(P, dims):
-    key = (P, tuple(dims))
+
+def loopback(P, dims, kernel="chain"):
+    import os
+    key = (P, tuple(dims), kernel)
     if key not in _LB:
-        _LB[key] = ddl.Loopback(P, list(dims))
+        env = LB_KERNELS[kernel]
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            _LB[key] = ddl.Loopback(P, list(dims))
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
     return _LB[key]
 
 
@@ -58,33 +73,35 @@ def run_allreduce(lb, bufs, dtype, op):
     return [to_host(t) for t in dev]
 
 
-def check_allreduce(P, dims, dtype, op, n, algo, seed=1811):
+def check_allreduce(P, dims, dtype, op, n, algo, seed=1811, kernel="chain"):
     bufs = si.rank_buffers(dtype, KIND[dtype], n, P, seed=seed)
     want = oracle.allreduce(bufs, dims, dtype, op)
-    lb = loopback(P, dims)
+    lb = loopback(P, dims, kernel)
     lb.set_algo(algo, 1 << 40 if algo == ddl.ALGO_ONESHOT else 0)
     got = run_allreduce(lb, bufs, dtype, op)
     for r in range(P):
-        assert same_bits(got[r], want[r]), (P, dims, dtype, op, n, algo, r, first_diff(got[r], want[r]))
+        assert same_bits(got[r], want[r]), (P, dims, dtype, op, n, algo, kernel, r, first_diff(got[r], want[r]))
 
 
 CASES = [(P, dims) for P in (2, 3, 4, 6, 8, 16) for dims in factorisations(P)]
 
 
 @pytest.mark.parametrize("P,dims", CASES, ids=[f"P{P}-{'x'.join(map(str, d))}" for P, d in CASES])
-@pytest.mark.parametrize("algo", [ddl.ALGO_HIER, ddl.ALGO_ONESHOT], ids=["hier", "oneshot"])
-def test_allreduce_parity(P, dims, algo):
+@pytest.mark.parametrize("algo,kernel", [(ddl.ALGO_HIER, "chain"), (ddl.ALGO_HIER, "slice"), (ddl.ALGO_ONESHOT, "chain")],
+                         ids=["hier-chain", "hier-slice", "oneshot"])
+def test_allreduce_parity(P, dims, algo, kernel):
     sizes = [1, P - 1 if P > 1 else 1, 1000, 40_003]
     for dtype in ("int32", "float32", "bfloat16"):
         for op in (["sum"] if dtype == "int32" else ["sum", "avg"]):
             for n in sizes:
-                check_allreduce(P, dims, dtype, op, n, algo)
+                check_allreduce(P, dims, dtype, op, n, algo, kernel=kernel)
 
 
+@pytest.mark.parametrize("kernel", sorted(LB_KERNELS))
 @pytest.mark.parametrize("P,dims", [(4, [2, 2]), (8, [2, 2, 2]), (8, [8]), (6, [3, 2])])
-def test_allreduce_large_ragged(P, dims):
+def test_allreduce_large_ragged(P, dims, kernel):
     for dtype in ("int32", "float32", "bfloat16"):
-        check_allreduce(P, dims, dtype, "sum" if dtype == "int32" else "avg", 1_000_003, ddl.ALGO_HIER)
+        check_allreduce(P, dims, dtype, "sum" if dtype == "int32" else "avg", 1_000_003, ddl.ALGO_HIER, kernel=kernel)
 
 
 def test_auto_algo_switch_is_invisible():
@@ -283,7 +300,7 @@ def test_kernel_paths_parity(path, P, dims):
     """Every hierarchical kernel variant (register-staged, TMA-staged for all sizes, work
     stealing, rank-level dynamic, streaming, waves) computes the same bits as the oracle."""
     import os
-    envs = PATH_ENVS[path]
+    envs = dict(PATH_ENVS[path], DDL_LB_CHAIN="0")  # variants of the slice kernels
     if path in EXPERIMENTAL_PATHS and not ddl.has_experimental_kernels():
         pytest.skip("PATH 3/4 experiment kernels not compiled (DDL_EXPERIMENTAL=1 bash build.sh)")
     old = {k: os.environ.get(k) for k in envs}
