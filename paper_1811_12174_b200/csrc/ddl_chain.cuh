@@ -59,6 +59,15 @@ namespace ddl {
 #define DDL_CHAIN_VPT 1
 #endif
 constexpr int kChainVPT = DDL_CHAIN_VPT;
+#ifndef DDL_CHAIN_PF  // BMAJOR loop: L2 prefetch of the first-phase sources this many grid strides ahead (0 off)
+#define DDL_CHAIN_PF 0
+#endif
+#ifndef DDL_CHAIN_PF_BULK
+#define DDL_CHAIN_PF_BULK 0
+#endif
+#ifndef DDL_CHAIN_SPLIT
+#define DDL_CHAIN_SPLIT 0
+#endif
 #ifndef DDL_CHAIN_FLAT
 #define DDL_CHAIN_FLAT 0
 #endif
@@ -264,6 +273,9 @@ __device__ __forceinline__ void static_for(F&& f) {
 // buffer base[r]), run in lockstep: each phase issues the loads of all NB columns before any of
 // their folds / stores, so a thread has NB independent chains in flight (NB x the memory-level
 // parallelism of one column, at NB x the registers).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
@@ -351,6 +363,57 @@ struct CTCols {
     }
   }
 
+  // Split form (DDL_CHAIN_SPLIT, NB = 1): an RS phase writer by writer (its g_d sources loaded,
+  // folded, stored, then the next writer) and an AG phase holder by holder (each receiver's load
+  // of the holder's copy, then their stores): at most max(g_d) values in registers instead of
+  // P / G_d, so more threads fit an SM (the column chain is latency-bound).
+  template <int li>
+  __device__ __forceinline__ static void rs_split(const CParams& p, char* const* base, size_t off) {
+    constexpr int g = TP::g(li), Gd = TP::G(li), Gd1 = TP::G(li + 1);
+    constexpr int sb = B0 % Gd, wb = B0 % Gd1;
+    constexpr bool last = li == TP::L - 1;
+#pragma unroll
+    for (int j = 0; j < P / Gd1; ++j) {
+      Raw raw[g];
+#pragma unroll
+      for (int v = 0; v < g; ++v)
+        raw[v] = IO::ld(base[sb + (v + j * g) * Gd] + off, li == 0 ? DDL_CHAIN_FIRST : DDL_CHAIN_REREAD);
+      A acc[N];
+      IO::unpack_(raw[0], acc);
+#pragma unroll
+      for (int v = 1; v < g; ++v) {
+        A y[N];
+        IO::unpack_(raw[v], y);
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc[k] = Tr<T>::add(acc[k], y[k]);
+      }
+      if (last && p.op == kAvg) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc[k] = Tr<T>::mul(acc[k], p.scale);
+      }
+      IO::st(base[wb + j * Gd1] + off, IO::pack_(acc), last && DDL_CHAIN_FINCS);
+    }
+  }
+  template <int li>
+  __device__ __forceinline__ static void ag_split(char* const* base, size_t off) {
+    constexpr int g = TP::g(li), Gd = TP::G(li), Gd1 = TP::G(li + 1);
+    constexpr int sb = B0 % Gd, beta = (B0 / Gd) % g;
+#pragma unroll
+    for (int j = 0; j < P / Gd1; ++j) {
+      Raw raw[g];
+#pragma unroll
+      for (int v = 0; v < g; ++v)
+        if (v != beta) raw[v] = IO::ld(base[sb + (beta + j * g) * Gd] + off, DDL_CHAIN_REREAD);
+#pragma unroll
+      for (int v = 0; v < g; ++v)
+        if (v != beta) IO::st(base[sb + (v + j * g) * Gd] + off, raw[v], DDL_CHAIN_FINCS);
+    }
+  }
+  __device__ __forceinline__ static void run_split(const CParams& p, char* const* base, size_t off) {
+    static_for<0, TP::L>([&](auto lc) { rs_split<decltype(lc)::value>(p, base, off); });
+    static_for<0, TP::L>([&](auto lc) { ag_split<TP::L - 1 - decltype(lc)::value>(base, off); });
+  }
+
   // every phase after the first RS phase's fold
   __device__ __forceinline__ static void after_first(const CParams& p, char* const* base, size_t off, uint64_t qb) {
     static_for<1, TP::L>([&](auto lc) { rs<decltype(lc)::value>(p, base, off, qb); });
@@ -396,9 +459,13 @@ struct CTCols {
     after_first(p, base, off, qb);
    }
 #else
-    // reduce-scatter phases (a4), live dims ascending; the last fuses the epilogue (a5)
-    rs<0>(p, base, off, qb);
-    after_first(p, base, off, qb);
+    if constexpr (DDL_CHAIN_SPLIT && NB == 1) {
+      run_split(p, base, off);
+    } else {
+      // reduce-scatter phases (a4), live dims ascending; the last fuses the epilogue (a5)
+      rs<0>(p, base, off, qb);
+      after_first(p, base, off, qb);
+    }
 #endif
   }
 };
@@ -486,6 +553,25 @@ __global__ void __launch_bounds__(kChainThreads, DDL_CHAIN_CT_MINB) ddl_chain_ct
       while (kb + 1 < p.nb && v >= p.b[kb + 1].row0) ++kb;
       const uint64_t qb = p.b[kb].q * sizeof(T);
       const uint64_t off = (uint64_t)(v - p.b[kb].row0) * 16u + b * qb;
+#if DDL_CHAIN_PF
+      // L2 prefetch of the first RS phase's sources DDL_CHAIN_PF grid strides ahead (same
+      // buffer only): no registers held, the later loads find them in L2
+      {
+        const uint32_t vn = v + DDL_CHAIN_PF * stride;
+        if (vn < (kb + 1 < p.nb ? p.b[kb + 1].row0 : p.nrows)) {
+          const uint64_t offn = off + (uint64_t)DDL_CHAIN_PF * stride * 16u;
+#if DDL_CHAIN_PF_BULK  // one lane per warp: a bulk L2 prefetch of the warp's 512 B per rank
+          if ((threadIdx.x & 31) == 0)
+#pragma unroll
+            for (int i = 0; i < P; ++i)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;" ::"l"(s_buf[kb][i] + offn) : "memory");
+#else
+#pragma unroll
+          for (int i = 0; i < P; ++i) asm volatile("prefetch.global.L2 [%0];" ::"l"(s_buf[kb][i] + offn));
+#endif
+        }
+      }
+#endif
       CTCols<T, TP, b, 1>::run(p, s_buf[kb], off, qb);
     }
   });
@@ -524,6 +610,128 @@ __global__ void __launch_bounds__(kChainThreads, DDL_CHAIN_CT_MINB) ddl_chain_ct
     const uint32_t b = lc / tail_rows;
     const uint64_t e0 = (uint64_t)b * B.q + (uint64_t)(B.vfull + (lc - b * tail_rows)) * W;
     if (e0 < B.n) chain_cold<T, P>(p, s_buf[k], b, e0, B.n);
+  }
+}
+
+// ------------------------------------------------------------------------ TMA-fed column chain
+// DDL_CHAIN_TMA: the CT kernel with the first RS phase's loads (the HBM reads) moved off the
+// threads: a producer warp bulk-copies (cp.async.bulk) the P ranks' segments of a tile --
+// kTmaCons consecutive full rows of one block b -- into a kTmaStages-deep shared-memory ring;
+// each of the kTmaCons consumer threads takes its column's P sources from the ring, folds and
+// stores them (RS phase 0), releases the stage, and runs the later phases with LDG / STG as in
+// ddl_chain_ct_kernel.  The reads in flight then cost no registers and no L1 miss slots.
+#ifndef DDL_CHAIN_TMA_DEFAULT  // loopback default: the TMA-fed kernel (1) or the LDG one (0)
+#define DDL_CHAIN_TMA_DEFAULT 1
+#endif
+#ifndef DDL_CHAIN_TMA_CONS
+#define DDL_CHAIN_TMA_CONS 512
+#endif
+#ifndef DDL_CHAIN_TMA_STAGES
+#define DDL_CHAIN_TMA_STAGES 2
+#endif
+constexpr int kTmaCons = DDL_CHAIN_TMA_CONS;
+constexpr int kTmaStages = DDL_CHAIN_TMA_STAGES;
+template <int P>
+constexpr size_t chain_tma_smem() {
+  return (size_t)kTmaStages * P * kTmaCons * 16 + 2 * kTmaStages * sizeof(uint64_t);
+}
+
+template <typename T, class TP>
+__global__ void __launch_bounds__(kTmaCons + 32, 1) ddl_chain_tma_kernel(const __grid_constant__ CParams p) {
+  constexpr int W = Tr<T>::W;
+  constexpr int P = TP::P;
+  constexpr uint32_t SEG = kTmaCons * 16;  // bytes of one rank's segment of a tile
+  using Raw = typename ColIO<T, true>::R;
+  extern __shared__ __align__(128) char dsm[];
+  char* ring = dsm;  // [stage][rank][SEG]
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)kTmaStages * P * SEG);
+  uint64_t* empty = full + kTmaStages;
+  __shared__ char* s_buf[kMaxBuckets][kMaxRanks];
+  __shared__ uint32_t s_ch0[kMaxBuckets + 1];  // first chunk (kTmaCons full rows) of each buffer
+  for (int i = threadIdx.x; i < p.nb * kMaxRanks; i += blockDim.x)
+    s_buf[i / kMaxRanks][i % kMaxRanks] = p.b[i / kMaxRanks].buf[i % kMaxRanks];
+  if (threadIdx.x == 0) {
+    uint32_t c = 0;
+    for (int k = 0; k < p.nb; ++k) {
+      s_ch0[k] = c;
+      c += (p.b[k].vfull + kTmaCons - 1) / kTmaCons;
+    }
+    s_ch0[p.nb] = c;
+    for (int st = 0; st < kTmaStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kTmaCons / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_begin();
+  const uint32_t C = s_ch0[p.nb];
+  const uint32_t ntiles = (uint32_t)P * C;
+  // tile t: block b = t / C (block-major), chunk t % C -> buffer k, rows [r0, r0 + rn)
+  auto tile_of = [&](uint32_t t, int& b, int& k, uint32_t& r0, uint32_t& rn) {
+    b = (int)(t / C);
+    const uint32_t ci = t - (uint32_t)b * C;
+    k = 0;
+    while (k + 1 < p.nb && ci >= s_ch0[k + 1]) ++k;
+    r0 = (ci - s_ch0[k]) * kTmaCons;
+    rn = min((uint32_t)kTmaCons, p.b[k].vfull - r0);
+  };
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == kTmaCons / 32) {  // producer warp
+    if (lane == 0) {
+      uint32_t i = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int st = (int)(i % kTmaStages);
+        if (i >= (uint32_t)kTmaStages) mbar_wait(&empty[st], ((i / kTmaStages) - 1) & 1u);
+        int b, k;
+        uint32_t r0, rn;
+        tile_of(t, b, k, r0, rn);
+        const uint64_t qb = p.b[k].q * sizeof(T);
+        mbar_arm(&full[st], (uint32_t)P * rn * 16u);
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+          tma_load(ring + ((size_t)st * P + r) * SEG, s_buf[k][r] + (uint64_t)b * qb + (uint64_t)r0 * 16u, rn * 16u,
+                   &full[st]);
+      }
+    }
+    return;
+  }
+  uint32_t i = 0;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    const int st = (int)(i % kTmaStages);
+    int b, k;
+    uint32_t r0, rn;
+    tile_of(t, b, k, r0, rn);
+    const uint64_t qb = p.b[k].q * sizeof(T);
+    const bool mine = (uint32_t)threadIdx.x < rn;
+    const uint64_t off = (uint64_t)b * qb + (uint64_t)(r0 + threadIdx.x) * 16u;
+    mbar_wait(&full[st], (i / kTmaStages) & 1u);
+    static_for<0, P>([&](auto bc) {
+      constexpr int B = decltype(bc)::value;
+      if (b != B) return;
+      using Cl = CTCols<T, TP, B, 1>;
+      typename Cl::template RawPh<0> raw;
+      if (mine) {
+#pragma unroll
+        for (int r = 0; r < P; ++r) raw[0][r] = reinterpret_cast<const Raw*>(ring + ((size_t)st * P + r) * SEG)[threadIdx.x];
+        Cl::template rs_fold<0>(p, s_buf[k], off, qb, raw);  // consumes raw: the stage is free
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (mine) Cl::after_first(p, s_buf[k], off, qb);
+    });
+  }
+  // the rest: rows vfull .. vq-1 of every buffer, one column (b, v) per consumer step
+  const uint32_t cstride = gridDim.x * kTmaCons;
+  int k = 0;
+  for (uint32_t c = blockIdx.x * kTmaCons + threadIdx.x; c < p.ncols; c += cstride) {
+    while (k + 1 < p.nb && c >= p.b[k + 1].col0) ++k;
+    const CBucket& Bk = p.b[k];
+    const uint32_t tail_rows = Bk.vq - Bk.vfull;
+    const uint32_t lc = c - Bk.col0;
+    const uint32_t b = lc / tail_rows;
+    const uint64_t e0 = (uint64_t)b * Bk.q + (uint64_t)(Bk.vfull + (lc - b * tail_rows)) * W;
+    if (e0 < Bk.n) chain_cold<T, P>(p, s_buf[k], b, e0, Bk.n);
   }
 }
 

@@ -170,6 +170,7 @@ struct ddl_comm {
                            // per-CTA slice kernels with device barriers, as across processes)
   int chain_hint = 0;      // DDL_CHAIN_HINTS: CParams::hint bits (generic chain kernel)
   bool chain_generic = false;  // DDL_CHAIN_GENERIC=1: the generic chain kernel also where a CT kernel exists
+  bool chain_tma = DDL_CHAIN_TMA_DEFAULT != 0;  // DDL_CHAIN_TMA: the TMA-fed CT kernel (ddl_chain.cuh)
 
   uint32_t* flags_of(int r) const {
     if (loopback) return reinterpret_cast<uint32_t*>(lb_flags + (size_t)r * flags_bytes);
@@ -297,6 +298,7 @@ void apply_env(ddl_comm* c) {
   c->lb_chain = (int)env_size("DDL_LB_CHAIN", c->lb_chain);
   c->chain_hint = (int)env_size("DDL_CHAIN_HINTS", c->chain_hint);
   c->chain_generic = env_size("DDL_CHAIN_GENERIC", 0) != 0;
+  c->chain_tma = env_size("DDL_CHAIN_TMA", c->chain_tma ? 1 : 0) != 0;
   if (c->stream_every < 1) c->stream_every = 1;
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
@@ -684,6 +686,27 @@ const void* chain_ct_t(const Topo& t) {
   return nullptr;
 }
 template <typename T>
+const void* chain_tma_t(const Topo& t) {
+  int g[4] = {1, 1, 1, 1};
+  const int L = t.nlive;
+  if (L < 1 || L > 4) return nullptr;
+  for (int l = 0; l < L; ++l) g[l] = t.g[t.live[l]];
+#define DDL_CT(L_, a, b, c, d)                                               \
+  if (L == L_ && g[0] == a && g[1] == b && g[2] == c && g[3] == d)          \
+    return (const void*)ddl_chain_tma_kernel<T, CT<L_, a, b, c, d>>;
+  DDL_CT(1, 2, 1, 1, 1)
+  DDL_CT(1, 4, 1, 1, 1) DDL_CT(2, 2, 2, 1, 1)
+  DDL_CT(1, 8, 1, 1, 1) DDL_CT(2, 4, 2, 1, 1) DDL_CT(2, 2, 4, 1, 1) DDL_CT(3, 2, 2, 2, 1)
+#undef DDL_CT
+  return nullptr;
+}
+const void* chain_tma_dt(ddl_dtype_t dt, const Topo& t) {
+  if (dt == DDL_INT32) return chain_tma_t<int32_t>(t);
+  if (dt == DDL_FLOAT32) return chain_tma_t<float>(t);
+  return chain_tma_t<__nv_bfloat16>(t);
+}
+
+template <typename T>
 const void* chain_fn_t(const Topo& t, bool generic, bool* ct) {
   if (!generic) {
     if (const void* f = chain_ct_t<T>(t)) {
@@ -709,6 +732,10 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
                                  ddl_op_t op, void* stream) {
   bool ct = false;
   const void* fn = chain_fn_dt(dt, c->topo, c->chain_generic, &ct);
+  // TMA-fed variant of the compile-time-topology kernel (DDL_CHAIN_TMA)
+  const void* tfn = (ct && c->chain_tma) ? chain_tma_dt(dt, c->topo) : nullptr;
+  const size_t tsmem = (size_t)kTmaStages * c->P * kTmaCons * 16 + 2 * kTmaStages * sizeof(uint64_t);
+  if (tfn) fn = tfn;
   const int w = elem_size(dt);
   const uint64_t W = 16 / w;
   const uint64_t kMaxCols = 1ull << 31;
@@ -747,14 +774,17 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
     cp.ncols = (uint32_t)cols;
     cp.nrows = (uint32_t)rows;
     if (!cols && !rows) continue;
-    const uint64_t need = (std::max(rows / kChainVPT, ct ? 0 : cols) + kChainThreads - 1) / kChainThreads;
-    const uint64_t cap = (uint64_t)blocks_per_sm(fn, 0, kChainThreads) * c->num_sms;
+    const int threads = tfn ? kTmaCons + 32 : kChainThreads;
+    const size_t smem = tfn ? tsmem : 0;
+    const uint64_t need = tfn ? (uint64_t)c->P * ((rows + kTmaCons - 1) / kTmaCons + cp.nb)
+                              : (std::max(rows / kChainVPT, ct ? 0 : cols) + kChainThreads - 1) / kChainThreads;
+    const uint64_t cap = (uint64_t)blocks_per_sm(fn, smem, threads) * c->num_sms;
     const int grid = (int)std::max<uint64_t>(1, std::min(need, c->ctas_limit > 0 ? (uint64_t)c->ctas_limit : cap));
     if (c->debug)
       std::fprintf(stderr, "[ddl] chain%s: %d buffers, %llu columns, grid %d\n", ct ? " (ct)" : "", cp.nb,
                    (unsigned long long)cols, grid);
     void* args[] = {&cp};
-    DDL_CUDA(launch_ex(fn, dim3(grid), 0, static_cast<cudaStream_t>(stream), args, false, c->use_pdl, kChainThreads));
+    DDL_CUDA(launch_ex(fn, dim3(grid), smem, static_cast<cudaStream_t>(stream), args, false, c->use_pdl, threads));
   }
   return DDL_SUCCESS;
 }

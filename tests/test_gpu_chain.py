@@ -19,8 +19,8 @@ from paper_1811_12174_b200 import ddl
 pytestmark = pytest.mark.gpu
 
 KIND = {"int32": "fullrange", "float32": "normal", "bfloat16": "normal"}
-KERNELS = {"ct": {"DDL_LB_CHAIN": "1"}, "generic": {"DDL_LB_CHAIN": "1", "DDL_CHAIN_GENERIC": "1"},
-           "slice": {"DDL_LB_CHAIN": "0"}}
+KERNELS = {"ct": {"DDL_LB_CHAIN": "1", "DDL_CHAIN_TMA": "0"}, "tma": {"DDL_LB_CHAIN": "1", "DDL_CHAIN_TMA": "1"},
+           "generic": {"DDL_LB_CHAIN": "1", "DDL_CHAIN_GENERIC": "1"}, "slice": {"DDL_LB_CHAIN": "0"}}
 
 
 def make_lb(P, dims, kernel):
@@ -62,7 +62,7 @@ TOPOS = [(2, [2]), (4, [4]), (4, [2, 2]), (8, [8]), (8, [4, 2]), (8, [2, 4]), (8
          (8, [4, 1, 2]), (6, [3, 2]), (12, [3, 4]), (16, [4, 4]), (16, [2, 2, 2, 2])]
 
 
-@pytest.mark.parametrize("kernel", ["ct", "generic"])
+@pytest.mark.parametrize("kernel", ["ct", "tma", "generic"])
 @pytest.mark.parametrize("P,dims", TOPOS, ids=[f"P{P}-{'x'.join(map(str, d))}" for P, d in TOPOS])
 def test_chain_matches_oracle_edge_sizes(P, dims, kernel):
     lb = make_lb(P, dims, kernel)
@@ -88,14 +88,14 @@ def test_chain_equals_slice_kernels_bitwise(P, dims):
         n = 3_000_017
         bufs = si.rank_buffers(dtype, KIND[dtype], n, P, seed=99)
         outs = {k: run(lb, bufs, dtype, op) for k, lb in lbs.items()}
-        for k in ("ct", "generic"):
+        for k in ("ct", "tma", "generic"):
             for r in range(P):
                 assert same_bits(outs[k][r], outs["slice"][r]), (k, dims, dtype, r, first_diff(outs[k][r], outs["slice"][r]))
     for lb in lbs.values():
         lb.finalize()
 
 
-@pytest.mark.parametrize("kernel", ["ct", "generic"])
+@pytest.mark.parametrize("kernel", ["ct", "tma", "generic"])
 def test_chain_grouped_many_buckets(kernel):
     """Grouped calls through the chain kernel: 11 buckets (two launches of <= 8), ragged and
     one-shot-sized ones mixed in, every bucket vs the oracle; and a CUDA-graph replay."""
