@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(kChainThreads, DDL_CHAIN_CT_MINB) ddl_chain_ct
 #define DDL_CHAIN_TMA_DEFAULT 1
 #endif
 #ifndef DDL_CHAIN_TMA_CONS
-#define DDL_CHAIN_TMA_CONS 512
+#define DDL_CHAIN_TMA_CONS 320
 #endif
 #ifndef DDL_CHAIN_TMA_STAGES
 #define DDL_CHAIN_TMA_STAGES 2
