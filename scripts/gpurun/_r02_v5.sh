@@ -1,5 +1,5 @@
 set -x
-TAG=${TAG:-r02_v1}
+TAG=${TAG:-r02_v5}
 mkdir -p gpurun_out
 python -c "import bench; print(bench.source_hash())" > gpurun_out/${TAG}_srchash.txt
 timeout 1500 python -m pytest tests -m gpu -q --timeout 600 2>&1 | tail -4 > gpurun_out/${TAG}_pytest_gpu.txt
