@@ -168,7 +168,6 @@ struct ddl_comm {
   int stream_every = 1;    // DDL_STREAM_EVERY (PATH 5)
   int lb_chain = 1;        // DDL_LB_CHAIN: loopback all-reduces through the column-chain kernel (0: the
                            // per-CTA slice kernels with device barriers, as across processes)
-  int chain_hint = 0;      // DDL_CHAIN_HINTS: CParams::hint bits (generic chain kernel)
   bool chain_generic = false;  // DDL_CHAIN_GENERIC=1: the generic chain kernel also where a CT kernel exists
   bool chain_tma = DDL_CHAIN_TMA_DEFAULT != 0;  // DDL_CHAIN_TMA: the TMA-fed CT kernel (ddl_chain.cuh)
 
@@ -296,7 +295,6 @@ void apply_env(ddl_comm* c) {
   c->debug = std::getenv("DDL_DEBUG") != nullptr;
   c->stream_every = (int)env_size("DDL_STREAM_EVERY", 1);
   c->lb_chain = (int)env_size("DDL_LB_CHAIN", c->lb_chain);
-  c->chain_hint = (int)env_size("DDL_CHAIN_HINTS", c->chain_hint);
   c->chain_generic = env_size("DDL_CHAIN_GENERIC", 0) != 0;
   c->chain_tma = env_size("DDL_CHAIN_TMA", c->chain_tma ? 1 : 0) != 0;
   if (c->stream_every < 1) c->stream_every = 1;
@@ -734,7 +732,7 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
   const void* fn = chain_fn_dt(dt, c->topo, c->chain_generic, &ct);
   // TMA-fed variant of the compile-time-topology kernel (DDL_CHAIN_TMA)
   const void* tfn = (ct && c->chain_tma) ? chain_tma_dt(dt, c->topo) : nullptr;
-  const size_t tsmem = (size_t)kTmaStages * c->P * kTmaCons * 16 + 2 * kTmaStages * sizeof(uint64_t);
+  const size_t tsmem = chain_tma_smem(c->P);
   if (tfn) fn = tfn;
   const int w = elem_size(dt);
   const uint64_t W = 16 / w;
@@ -746,7 +744,6 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
     cp.t = c->topo;
     cp.op = op;
     cp.scale = 1.0f / (float)c->P;  // fl32(1/P)
-    cp.hint = c->chain_hint;
     uint64_t cols = 0, rows = 0;
     while (i < nb && cp.nb < kMaxBuckets) {
       const uint64_t n = ns[i];
@@ -755,7 +752,7 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
       // CT kernels: rows v < vfull have a whole vector in every block (the last block holds
       // n - (P-1) q elements); the other rows' columns go through the generic column code
       const uint64_t last = n > (uint64_t)(c->P - 1) * q ? n - (uint64_t)(c->P - 1) * q : 0;
-      const uint64_t vfull = ct ? std::min<uint64_t>(vq, last / W) / kChainVPT * kChainVPT : 0;
+      const uint64_t vfull = ct ? std::min<uint64_t>(vq, last / W) : 0;
       const uint64_t bc = (uint64_t)c->P * (vq - vfull);
       if (bc > kMaxCols || vfull > kMaxCols) return DDL_ERR_TOO_LARGE;
       if (cols + bc > kMaxCols || rows + vfull > kMaxCols) break;
@@ -777,7 +774,7 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
     const int threads = tfn ? kTmaCons + 32 : kChainThreads;
     const size_t smem = tfn ? tsmem : 0;
     const uint64_t need = tfn ? (uint64_t)c->P * ((rows + kTmaCons - 1) / kTmaCons + cp.nb)
-                              : (std::max(rows / kChainVPT, ct ? 0 : cols) + kChainThreads - 1) / kChainThreads;
+                              : (std::max(rows, ct ? 0 : cols) + kChainThreads - 1) / kChainThreads;
     const uint64_t cap = (uint64_t)blocks_per_sm(fn, smem, threads) * c->num_sms;
     const int grid = (int)std::max<uint64_t>(1, std::min(need, c->ctas_limit > 0 ? (uint64_t)c->ctas_limit : cap));
     if (c->debug)
