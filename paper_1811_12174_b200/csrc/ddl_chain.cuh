@@ -47,6 +47,11 @@ namespace ddl {
 // profiles/r02_ab/r02_chain*.txt: the first RS phase's loads (HBM) .cg, the later phases'
 // re-reads of the column's own partials / finals .ca (L1 hits: the thread stored them a few
 // instructions earlier), final stores default (DDL_CHAIN_FINCS=1: .cs).
+// Why .ca is safe although L1 is not coherent across SMs: a re-read only ever targets bytes
+// the same thread stored earlier in this launch (every column belongs to exactly one thread),
+// and a thread's own stores are visible to its later loads through its SM's L1 (write-
+// through); bytes of other columns that share the 128-B line may be stale in this L1, but no
+// thread of this SM ever reads them, and L1 is invalidated at every launch.
 #ifndef DDL_CHAIN_FIRST
 #define DDL_CHAIN_FIRST 0
 #endif
@@ -187,7 +192,7 @@ __device__ __forceinline__ void chain_column(const CParams& p, char* const* buf,
 #pragma unroll
         for (int k = 0; k < N; ++k) acc[k] = v == 0 ? y[k] : Tr<T>::add(acc[k], y[k]);
         if (++v == g) {
-          if (last && p.op == kAvg) {
+          if (last && p.op == kAvg && DDL_MUTATE != 8) {  // mutation 8: generic kernel drops the 1/P scale
 #pragma unroll
             for (int k = 0; k < N; ++k) acc[k] = Tr<T>::mul(acc[k], p.scale);
           }
@@ -299,15 +304,21 @@ struct CTCol {
 #pragma unroll
     for (int j = 0; j < P / Gd1; ++j) {  // writer wb + j*Gd1 folds members v = 0..g-1 (source v + j*g)
       A acc[N];
+#if DDL_MUTATE == 4  // mutation check (scripts/gpu_mutation_check.sh): members folded in descending order
+      IO::unpack_(raw[j * g + g - 1], acc);
+#pragma unroll
+      for (int v = g - 2; v >= 0; --v) {
+#else
       IO::unpack_(raw[j * g], acc);
 #pragma unroll
       for (int v = 1; v < g; ++v) {
+#endif
         A y[N];
         IO::unpack_(raw[j * g + v], y);
 #pragma unroll
         for (int k = 0; k < N; ++k) acc[k] = Tr<T>::add(acc[k], y[k]);
       }
-      if (last && p.op == kAvg) {
+      if (last && p.op == kAvg && DDL_MUTATE != 5) {  // mutation 5: the fused 1/P scale dropped
 #pragma unroll
         for (int k = 0; k < N; ++k) acc[k] = Tr<T>::mul(acc[k], p.scale);
       }
@@ -325,7 +336,8 @@ struct CTCol {
       if (i % g != beta) raw[i] = IO::ld(base[sb + (i - i % g + beta) * Gd] + off, DDL_CHAIN_REREAD);
 #pragma unroll
     for (int i = 0; i < n; ++i)
-      if (i % g != beta) IO::st(base[sb + i * Gd] + off, raw[i], DDL_CHAIN_FINCS);
+      if (i % g != beta && !(DDL_MUTATE == 6 && li == 0 && i == n - 1 - (beta == n - 1)))  // mutation 6: a receiver skipped
+        IO::st(base[sb + i * Gd] + off, raw[i], DDL_CHAIN_FINCS);
   }
   // every phase after the first RS phase's fold
   __device__ __forceinline__ static void after_first(const CParams& p, char* const* base, size_t off) {
@@ -402,19 +414,23 @@ __global__ void __launch_bounds__(kChainThreads, DDL_CHAIN_CT_MINB) ddl_chain_ct
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// ring stages for P ranks: kTmaStages at P = 8, more for smaller P so that the ring (the bytes
+// in flight per CTA) stays at kTmaStages x 8 x kTmaCons x 16 B
+__host__ __device__ constexpr int chain_tma_stages(int P) { return P >= 8 ? kTmaStages : kTmaStages * (8 / P); }
 inline size_t chain_tma_smem(int P) {
-  return (size_t)kTmaStages * P * kTmaCons * 16 + 2 * kTmaStages * sizeof(uint64_t);
+  return (size_t)chain_tma_stages(P) * P * kTmaCons * 16 + 2 * chain_tma_stages(P) * sizeof(uint64_t);
 }
 
 template <typename T, class TP>
 __global__ void __launch_bounds__(kTmaCons + 32, DDL_CHAIN_TMA_MINB) ddl_chain_tma_kernel(const __grid_constant__ CParams p) {
   constexpr int P = TP::P;
+  constexpr int S = chain_tma_stages(P);
   constexpr uint32_t SEG = kTmaCons * 16;  // bytes of one rank's segment of a tile
   using Raw = typename ColIO<T, true>::R;
   extern __shared__ __align__(128) char dsm[];
   char* ring = dsm;  // [stage][rank][SEG]
-  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)kTmaStages * P * SEG);
-  uint64_t* empty = full + kTmaStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)S * P * SEG);
+  uint64_t* empty = full + S;
   __shared__ ChainSmem s;
   __shared__ uint32_t s_ch0[kMaxBuckets + 1];  // first chunk (kTmaCons full rows) of each buffer
   load_ptrs(p, s);
@@ -425,7 +441,7 @@ __global__ void __launch_bounds__(kTmaCons + 32, DDL_CHAIN_TMA_MINB) ddl_chain_t
       c += (p.b[k].vfull + kTmaCons - 1) / kTmaCons;
     }
     s_ch0[p.nb] = c;
-    for (int st = 0; st < kTmaStages; ++st) {
+    for (int st = 0; st < S; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kTmaCons / 32);
     }
@@ -449,8 +465,8 @@ __global__ void __launch_bounds__(kTmaCons + 32, DDL_CHAIN_TMA_MINB) ddl_chain_t
     if (lane == 0) {
       uint32_t i = 0;
       for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-        const int st = (int)(i % kTmaStages);
-        if (i >= (uint32_t)kTmaStages) mbar_wait(&empty[st], ((i / kTmaStages) - 1) & 1u);
+        const int st = (int)(i % S);
+        if (i >= (uint32_t)S) mbar_wait(&empty[st], ((i / S) - 1) & 1u);
         int b, k;
         uint32_t r0, rn;
         tile_of(t, b, k, r0, rn);
@@ -466,14 +482,14 @@ __global__ void __launch_bounds__(kTmaCons + 32, DDL_CHAIN_TMA_MINB) ddl_chain_t
   }
   uint32_t i = 0;
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-    const int st = (int)(i % kTmaStages);
+    const int st = (int)(i % S);
     int b, k;
     uint32_t r0, rn;
     tile_of(t, b, k, r0, rn);
     const uint64_t qb = p.b[k].q * sizeof(T);
     const bool mine = (uint32_t)threadIdx.x < rn;
     const uint64_t off = (uint64_t)b * qb + (uint64_t)(r0 + threadIdx.x) * 16u;
-    mbar_wait(&full[st], (i / kTmaStages) & 1u);
+    mbar_wait(&full[st], (i / S) & 1u);
     static_for<0, P>([&](auto bc) {  // b is uniform over the CTA: one branch taken
       constexpr int B = decltype(bc)::value;
       if (b != B) return;
@@ -481,7 +497,8 @@ __global__ void __launch_bounds__(kTmaCons + 32, DDL_CHAIN_TMA_MINB) ddl_chain_t
       if (mine) {
         Raw raw[P];
 #pragma unroll
-        for (int r = 0; r < P; ++r) raw[r] = reinterpret_cast<const Raw*>(ring + ((size_t)st * P + r) * SEG)[threadIdx.x];
+        for (int r = 0; r < P; ++r)  // (mutation 7: two ranks' segments swapped)
+          raw[r] = reinterpret_cast<const Raw*>(ring + ((size_t)st * P + (DDL_MUTATE == 7 && (r == 1 || r == 2) ? 3 - r : r)) * SEG)[threadIdx.x];
         Cl::template rs_fold<0>(p, s.buf[k], off, raw);  // consumes raw: the stage is free
       }
       __syncwarp();

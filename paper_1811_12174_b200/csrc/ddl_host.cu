@@ -498,6 +498,8 @@ bool plan_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
 // Loopback runs it only when forced (ALGO_LL): all virtual ranks in one cooperative launch,
 // so the kernel can be profiled under kernel serialisation; AUTO keeps LL for the cross-GPU
 // latency regime it is built for.
+bool use_chain(const ddl_comm* c);
+
 bool use_ll(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
   if (c->P < 2 || c->check) return false;
   if (c->loopback && (c->algo != DDL_ALGO_LL || !c->lb_ll)) return false;
@@ -521,6 +523,9 @@ bool use_ll(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
 
 bool use_oneshot(const ddl_comm* c, uint64_t n, ddl_dtype_t dt, Plan* pl) {
   if (c->P < 2 || c->algo == DDL_ALGO_HIER) return false;
+  // loopback: the column-chain kernel beats the one-shot at every size (one launch, no
+  // barrier; 3.6 vs 13 us at 0.5-1 MiB, profiles/r02c_loopback_sweep.csv): AUTO never picks it
+  if (c->algo == DDL_ALGO_AUTO && use_chain(c)) return false;
   if (!c->loopback && n * (uint64_t)elem_size(dt) > c->scratch_half) return false;  // scratch-bound
   if (c->algo == DDL_ALGO_AUTO && n * (uint64_t)elem_size(dt) > c->oneshot_max) return false;
   return plan_oneshot(c, n, dt, pl);
