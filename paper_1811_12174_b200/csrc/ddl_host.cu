@@ -742,6 +742,9 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
   const int w = elem_size(dt);
   const uint64_t W = 16 / w;
   const uint64_t kMaxCols = 1ull << 31;
+  // every buffer must fit one launch's 31-bit column / row space: refuse before enqueuing any
+  for (int j = 0; j < nb; ++j)
+    if ((uint64_t)c->P * (block_elems(ns[j], c->P, w) / W) > kMaxCols) return DDL_ERR_TOO_LARGE;
   int i = 0;
   while (i < nb) {
     CParams cp;
