@@ -199,3 +199,43 @@ def test_no_write_outside_the_buffers(P, dims, kernel):
                 assert torch.equal(bk[r][G + n:].view(torch.uint8), g1.view(torch.uint8)), (kernel, dtype, n, r, "after")
                 assert same_bits(to_host(views[i][r]), want[r]), (kernel, dtype, n, r)
     lb.finalize()
+
+
+def test_first_call_inside_graph_capture(tmp_path):
+    """A fresh process whose FIRST loopback all-reduce is captured into a CUDA graph (kernel
+    loading, occupancy query and smem attribute happen during the capture): the replay is
+    bit-exact vs the oracle, for the TMA-fed chain kernel of 2x4 and the grouped call."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)
+import numpy as np, torch
+import oracle, synthetic_inputs as si
+from gpu_util import to_dev, to_host, same_bits
+from paper_1811_12174_b200 import ddl
+P, dims = 8, [4, 2]
+lb = ddl.Loopback(P, dims)
+sizes = [300_001, 65_536]
+bufs = [[torch.zeros(n, device="cuda") for _ in range(P)] for n in sizes]
+s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
+g = torch.cuda.CUDAGraph()
+with torch.cuda.stream(s):
+    with torch.cuda.graph(g, stream=s):
+        lb.all_reduce(bufs[0], "avg")
+        lb.all_reduce_many(bufs, "sum")
+torch.cuda.synchronize()
+hv = [si.rank_buffers("float32", "normal", n, P, seed=70 + i) for i, n in enumerate(sizes)]
+for b, h in zip(bufs, hv):
+    for r in range(P):
+        b[r].copy_(to_dev(h[r], "float32"))
+g.replay(); torch.cuda.synchronize()
+w0 = oracle.allreduce(oracle.allreduce(hv[0], dims, "float32", "avg"), dims, "float32", "sum")
+w1 = oracle.allreduce(hv[1], dims, "float32", "sum")
+assert lb.async_error() == ddl.SUCCESS
+assert all(same_bits(to_host(bufs[0][r]), w0[r]) for r in range(P))
+assert all(same_bits(to_host(bufs[1][r]), w1[r]) for r in range(P))
+print("capture ok")
+''' % (root, os.path.join(root, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "capture ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
