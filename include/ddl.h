@@ -280,9 +280,15 @@ ddl_result_t ddl_debug_register_local(ddl_comm_t* comms, void* const* ptrs, size
 ddl_result_t ddl_finalize(ddl_comm_t comm);
 
 /* ------------------------------------------------------------------ loopback (1 GPU) */
-/* P virtual ranks in ONE GPU's memory, all in one cooperative launch (deadlock-free):
- * the same kernels, barrier protocol and block layout as the multi-process path, with
- * "peer" pointers that are local.  Used by the parity tests and the 1-GPU benchmark. */
+/* P virtual ranks in ONE GPU's memory (used by the parity tests and the 1-GPU benchmark).
+ * All-reduces (ddl_group_allreduce, ddl_group_allreduce_many) run the column-chain kernels
+ * (csrc/ddl_chain.cuh): the schedule's RS / AG phases per column
+ * of every block in one thread, every load and store of the schedule, bit-identical results;
+ * no barrier is needed because a column's phases run in program order in that thread.  With
+ * DDL_LB_CHAIN=0 (or the debug hooks ddl_debug_skip_rank / DDL_TRACE) they run the
+ * multi-process path's slice kernels instead -- same block layout and barrier protocol, all
+ * P ranks in one cooperative launch (deadlock-free), "peer" pointers local -- as do the
+ * loopback reduce-scatter / allgather. */
 
 ddl_result_t ddl_loopback_init(ddl_comm_t* comm, int nranks, const int* dims, int ndims, int cuda_device);
 /* The same under SURVEY 8(b)'s name and argument list (max_bytes is unused: loopback calls
@@ -295,8 +301,9 @@ ddl_result_t ddl_init_loopback(ddl_comm_t* comm, int nranks, const int* dims, in
 ddl_result_t ddl_group_allreduce(ddl_comm_t comm, void* const* bufs, size_t count, ddl_dtype_t dtype,
                                  ddl_op_t op, void* stream);
 /* Grouped all-reduce in loopback: bufs[i * nranks + r] is virtual rank r's copy of buffer i
- * (counts[i] elements); otherwise as ddl_allreduce_many (one-shot-sized buffers by single
- * ddl_group_allreduce calls first, the rest in one cooperative launch per 8 buffers). */
+ * (counts[i] elements); otherwise as ddl_allreduce_many (one launch per 8 buffers; with the
+ * slice kernels, one-shot-sized buffers go through single ddl_group_allreduce calls first).
+ * DDL_ERR_TOO_LARGE (nothing enqueued) if a buffer exceeds 2^31 16-byte columns. */
 ddl_result_t ddl_group_allreduce_many(ddl_comm_t comm, void* const* bufs, const size_t* counts, int nbufs,
                                       ddl_dtype_t dtype, ddl_op_t op, void* stream);
 /* sendbufs[r]: nranks*recvcount elements (not modified); recvbufs[r]: recvcount.
