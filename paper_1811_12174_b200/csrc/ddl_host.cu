@@ -786,8 +786,8 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
     const uint64_t cap = (uint64_t)blocks_per_sm(fn, smem, threads) * c->num_sms;
     const int grid = (int)std::max<uint64_t>(1, std::min(need, c->ctas_limit > 0 ? (uint64_t)c->ctas_limit : cap));
     if (c->debug)
-      std::fprintf(stderr, "[ddl] chain%s: %d buffers, %llu columns, grid %d\n", ct ? " (ct)" : "", cp.nb,
-                   (unsigned long long)cols, grid);
+      std::fprintf(stderr, "[ddl] chain (%s): %d buffers, %llu full rows, %llu tail columns, grid %d\n",
+                   tfn ? "tma" : ct ? "ct" : "generic", cp.nb, (unsigned long long)rows, (unsigned long long)cols, grid);
     void* args[] = {&cp};
     DDL_CUDA(launch_ex(fn, dim3(grid), smem, static_cast<cudaStream_t>(stream), args, false, c->use_pdl, threads));
   }
