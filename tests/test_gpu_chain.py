@@ -239,3 +239,26 @@ print("capture ok")
 ''' % (root, os.path.join(root, "tests"))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "capture ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
+
+
+def test_bench_step_every_element_vs_oracle():
+    """bench.py N = 1's exact call -- Loopback(8, 2x4).all_reduce_many(the 5 ResNet-50
+    buckets, avg), 25.6 M fp32 per virtual rank, through the default (TMA-fed chain) kernel --
+    compared with the oracle on EVERY element of every bucket and rank (the oracle runs the
+    whole set in ~1 s), plus a second step on the reduced values."""
+    P, dims = 8, ddl.parse_dims("2x4")
+    lb = ddl.Loopback(P, dims, device=0)
+    nb = len(si.resnet50_bucket_bytes())
+    host = [[si.resnet50_bucket(b, r) for r in range(P)] for b in range(nb)]
+    bufs = [[to_dev(host[b][r], "float32") for r in range(P)] for b in range(nb)]
+    for step in range(2):
+        lb.all_reduce_many(bufs, "avg")
+        torch.cuda.synchronize()
+        assert lb.async_error() == ddl.SUCCESS
+        for b in range(nb):
+            want = oracle.allreduce(host[b], dims, "float32", "avg")
+            for r in range(P):
+                got = to_host(bufs[b][r])
+                assert same_bits(got, want[r]), (step, b, r, first_diff(got, want[r]))
+        host = [[w for w in oracle.allreduce(host[b], dims, "float32", "avg")] for b in range(nb)]
+    lb.finalize()
