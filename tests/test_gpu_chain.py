@@ -262,3 +262,21 @@ def test_bench_step_every_element_vs_oracle():
                 assert same_bits(got, want[r]), (step, b, r, first_diff(got, want[r]))
         host = [[w for w in oracle.allreduce(host[b], dims, "float32", "avg")] for b in range(nb)]
     lb.finalize()
+
+
+@pytest.mark.parametrize("P,spec", [(2, "2"), (4, "2x2"), (8, "2x2x2")])
+def test_config3_unet3d_every_element_vs_oracle(P, spec):
+    """BASELINE config 3 (3D U-Net gradient set, 19,075,523 fp32, avg) at P = 2 / 4 / 8 through
+    the default loopback kernel, every element of every rank vs the oracle."""
+    dims = ddl.parse_dims(spec)
+    lb = ddl.Loopback(P, dims, device=0)
+    host = [si.unet3d_gradients(r) for r in range(P)]
+    dev = [to_dev(h, "float32") for h in host]
+    lb.all_reduce(dev, "avg")
+    torch.cuda.synchronize()
+    assert lb.async_error() == ddl.SUCCESS
+    want = oracle.allreduce(host, dims, "float32", "avg")
+    for r in range(P):
+        got = to_host(dev[r])
+        assert same_bits(got, want[r]), (spec, r, first_diff(got, want[r]))
+    lb.finalize()
