@@ -508,8 +508,9 @@ def run_loopback(args):
                                      "(null unless that capture measured this build: source hash)",
                      "algorithmic_bytes_per_launch": algo_bytes // args.steps // launches_per_step,
                      "peak_source": peak_src,
-                     "kernel": "ddl_chain_ct_kernel<float, CT<2,4,2>> (loopback column chain: 5 buckets x 8 "
-                               "virtual ranks in one launch, every RS/AG phase per column in one thread)",
+                     "kernel": "ddl_chain_tma_kernel<float, CT<2,4,2>> (loopback column chain: 5 buckets x 8 "
+                               "virtual ranks in one launch, every RS/AG phase per column in one thread, "
+                               "first-phase sources staged by TMA bulk copies)",
                      "kernel_timing": ("CUDA events over the timed region, one launch per step (region / K)"
                                        if launches_per_step == 1 else
                                        "second pass of K steps, CUDA events around every launch"),
