@@ -28,12 +28,13 @@
 // read once and its result written once (the compulsory 2*P*S).
 //
 // Three kernels:
-//   ddl_chain_tma_kernel  (default; compile-time topology, P = 2/4/8) a producer warp
+//   ddl_chain_tma_kernel  (default for P = 4/8; compile-time topology, P = 2/4/8) a producer warp
 //       bulk-copies (TMA, cp.async.bulk) the first RS phase's sources of a tile -- kTmaCons
 //       consecutive columns of one block -- into a shared-memory ring; the consumer threads fold
 //       from it and run the later phases with LDG / STG.  The HBM reads in flight cost no
 //       registers and no L1 miss slots (profiles/r02_ab/r02_chain14-17.txt: 0.256 vs 0.296 ms).
-//   ddl_chain_ct_kernel   (DDL_CHAIN_TMA=0) the same with the first-phase loads as LDG.
+//   ddl_chain_ct_kernel   (default for P = 2, DDL_CHAIN_TMA=0 everywhere) the same with the
+//       first-phase loads as LDG.
 //   ddl_chain_kernel      (any P <= 16, DDL_CHAIN_GENERIC=1 everywhere) runtime topology, one
 //       column per thread.
 // Columns of several buffers (the grouped all-reduce of DDP buckets) are concatenated and
@@ -67,8 +68,8 @@ namespace ddl {
 #ifndef DDL_CHAIN_CT_MINB  // ... and the LDG compile-time-topology kernel (64 registers)
 #define DDL_CHAIN_CT_MINB 4
 #endif
-#ifndef DDL_CHAIN_TMA_DEFAULT  // loopback default: the TMA-fed kernel (1) or the LDG one (0)
-#define DDL_CHAIN_TMA_DEFAULT 1
+#ifndef DDL_CHAIN_TMA_DEFAULT  // loopback default: the TMA-fed kernel (1), the LDG one (0), or -1 = TMA from P = 4
+#define DDL_CHAIN_TMA_DEFAULT -1
 #endif
 #ifndef DDL_CHAIN_TMA_CONS  // TMA-fed kernel: consumer threads = columns per tile
 #define DDL_CHAIN_TMA_CONS 320

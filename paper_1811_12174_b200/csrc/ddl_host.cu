@@ -169,7 +169,9 @@ struct ddl_comm {
   int lb_chain = 1;        // DDL_LB_CHAIN: loopback all-reduces through the column-chain kernel (0: the
                            // per-CTA slice kernels with device barriers, as across processes)
   bool chain_generic = false;  // DDL_CHAIN_GENERIC=1: the generic chain kernel also where a CT kernel exists
-  bool chain_tma = DDL_CHAIN_TMA_DEFAULT != 0;  // DDL_CHAIN_TMA: the TMA-fed CT kernel (ddl_chain.cuh)
+  int chain_tma = DDL_CHAIN_TMA_DEFAULT;  // DDL_CHAIN_TMA: the TMA-fed CT kernel (ddl_chain.cuh): 1 on, 0 off,
+                                          // -1 auto = from P = 4 (at P = 2 the LDG form is as fast or
+                                          // faster: profiles/r02_ab/r02_p2_ab.txt)
 
   uint32_t* flags_of(int r) const {
     if (loopback) return reinterpret_cast<uint32_t*>(lb_flags + (size_t)r * flags_bytes);
@@ -296,7 +298,7 @@ void apply_env(ddl_comm* c) {
   c->stream_every = (int)env_size("DDL_STREAM_EVERY", 1);
   c->lb_chain = (int)env_size("DDL_LB_CHAIN", c->lb_chain);
   c->chain_generic = env_size("DDL_CHAIN_GENERIC", 0) != 0;
-  c->chain_tma = env_size("DDL_CHAIN_TMA", c->chain_tma ? 1 : 0) != 0;
+  if (const char* v = std::getenv("DDL_CHAIN_TMA")) c->chain_tma = *v ? (int)std::strtol(v, nullptr, 10) : c->chain_tma;
   if (c->stream_every < 1) c->stream_every = 1;
   if (const char* a = std::getenv("DDL_ALGO")) {
     if (!std::strcmp(a, "hier")) c->algo = DDL_ALGO_HIER;
@@ -736,7 +738,8 @@ ddl_result_t launch_chain(const ddl_comm* c, const uint64_t* ns, void* const* pt
   bool ct = false;
   const void* fn = chain_fn_dt(dt, c->topo, c->chain_generic, &ct);
   // TMA-fed variant of the compile-time-topology kernel (DDL_CHAIN_TMA)
-  const void* tfn = (ct && c->chain_tma) ? chain_tma_dt(dt, c->topo) : nullptr;
+  const bool tma = c->chain_tma > 0 || (c->chain_tma < 0 && c->P >= 4);
+  const void* tfn = (ct && tma) ? chain_tma_dt(dt, c->topo) : nullptr;
   const size_t tsmem = chain_tma_smem(c->P);
   if (tfn) fn = tfn;
   const int w = elem_size(dt);
